@@ -1,0 +1,155 @@
+/*
+ * rbffd_b200.h -- C ABI of the B200-native explicit RBF-FD time loop.
+ *
+ * This library replaces, for one NVIDIA B200 (sm_100a), the hot path of the
+ * reference package `rbffd` (arXiv 2107.03632, /root/reference/pkg):
+ *
+ *   rbffd.solver._step_kernel   pkg/src/rbffd/solver.py:294-311  (numba, the update)
+ *   rbffd.solver.run_time_loop  pkg/src/rbffd/solver.py:168-236  (the step loop,
+ *                               flag check :200-206, residual :208-211,
+ *                               swap/copy-back :212-215, steady break :216-217)
+ *   rbffd.solver.explicit_step  pkg/src/rbffd/solver.py:141-165  (one step)
+ *
+ * The reference has no FFI: its boundary is the Python call
+ *   _step_kernel(u1, u2, interior, rows, weights, f_int, dt, chunk, flags)
+ * (solver.py:294-295).  The functions below are the entry points a ctypes
+ * binding of that call binds.  Plain C types only.
+ *
+ * Arithmetic contract (bitwise parity with the reference): per interior row k,
+ *     acc = 0.0;  for j in 0..n-1: acc = acc + w[k,j]*u1[rows[k,j]]   (serial j)
+ *     u2[interior[k]] = u1[interior[k]] + dt*(f_int[k] + acc)
+ * every product and sum separately rounded (no FMA), exactly as the numba
+ * kernel compiles (solver.py:304-307).
+ *
+ * Status codes (int return of every call):
+ *     RBF_OK 0, RBF_ERR_CUDA 1, RBF_ERR_PARAM 2, RBF_ERR_INSTABILITY 4,
+ *     RBF_ERR_TIMEOUT 5.
+ * They map onto the reference exceptions (pkg/src/rbffd/errors.py):
+ *     2 -> ParameterError (:4), 4 -> InstabilityError(step, max_abs) (:21-27),
+ *     5 -> SteadyStateTimeout(steps, residual) (:30-36).
+ * rbf_last_error() returns a thread-local message for the last failure.
+ *
+ * Calls are synchronous.  A plan is not thread-safe: one plan per host thread.
+ */
+#ifndef RBFFD_B200_H
+#define RBFFD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RBF_OK 0
+#define RBF_ERR_CUDA 1
+#define RBF_ERR_PARAM 2
+#define RBF_ERR_INSTABILITY 4
+#define RBF_ERR_TIMEOUT 5
+
+/* plan flags */
+#define RBF_RENUMBER_MORTON 0x1u  /* locality renumbering of interior rows (needs positions) */
+#define RBF_NO_RESIDENT 0x2u      /* never use the on-chip (single-CTA) resident loop */
+#define RBF_NO_PDL 0x4u           /* disable programmatic dependent launch between steps */
+
+/* run modes (SolveConfig.mode, solver.py:53) */
+#define RBF_MODE_FIXED 0
+#define RBF_MODE_STEADY 1
+
+typedef struct rbf_plan rbf_plan;
+
+/*
+ * Build a plan on `device`: pack the reference's ShapeStore into the
+ * sliced-transposed ELL layout (SELL-32, fp64 weights, int32 node ids) and
+ * upload it.  Replaces the per-call array prep of run_time_loop
+ * (solver.py:181-190) and the layout of ShapeStore (weights.py:71-86) +
+ * StencilSet (neighborhoods.py:25-35).
+ *
+ *   N          total node count (NodeSet.n_total, geometry.py:53-55)
+ *   N_i        interior row count (ShapeStore.n_rows, weights.py:84-86)
+ *   n          support size (StencilSet.n)
+ *   interior   [N_i]    ShapeStore.interior_nodes (distinct node ids)
+ *   rows       [N_i*n]  stencils.neighbors[interior], row-major (solver.py:182)
+ *   weights    [N_i*n]  ShapeStore.weights, row-major
+ *   f_int      [N_i]    forcing at interior nodes (solver.py:184)
+ *   positions  [N*2]    node coordinates, only read with RBF_RENUMBER_MORTON (may be NULL)
+ * The caller keeps ownership of every host array.
+ */
+int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n,
+                    const int64_t* interior, const int64_t* rows,
+                    const double* weights, const double* f_int,
+                    const double* positions, int32_t device, uint32_t flags);
+
+/* Replace the per-row forcing (explicit_step's f[interior], solver.py:156). */
+int rbf_set_forcing(rbf_plan* plan, const double* f_int);
+
+/* Upload the full field u[N] (original node order) into both device buffers
+ * (run_time_loop: u1 = apply_dirichlet(...); u2 = u1.copy(), solver.py:186-187). */
+int rbf_set_field(rbf_plan* plan, const double* u_host);
+
+/* Download the current field u[N] in original node order.  After
+ * RBF_ERR_INSTABILITY this is the u2 of the failing step (solver.py:201). */
+int rbf_get_field(rbf_plan* plan, double* u_host);
+
+/*
+ * The time loop of run_time_loop (solver.py:191-225), on the device.
+ *   mode      RBF_MODE_FIXED: `steps` steps, residual of the last step only
+ *             RBF_MODE_STEADY: up to `max_steps` steps, residual every step,
+ *             stop when residual <= tol
+ *   copy_back 0 swap buffers (solver.py:215), 1 copy u2 into u1 (solver.py:213)
+ * Outputs: steps_done, residual (max|u2-u1|/dt, valid when *has_residual),
+ *   bad_step (first step with a non-finite value, -1 if none), device_seconds
+ *   (CUDA-event time of the loop).
+ * Returns RBF_ERR_INSTABILITY (bad_step set) or RBF_ERR_TIMEOUT like the
+ * reference raises InstabilityError / SteadyStateTimeout.
+ */
+int rbf_run(rbf_plan* plan, double dt, int64_t steps, int32_t mode, double tol,
+            int64_t max_steps, int32_t copy_back, int64_t* steps_done,
+            double* residual, int32_t* has_residual, int64_t* bad_step,
+            double* device_seconds);
+
+/* One explicit step on the resident field (explicit_step, solver.py:141-165);
+ * RBF_ERR_INSTABILITY if any updated value is non-finite. */
+int rbf_step(rbf_plan* plan, double dt);
+
+/*
+ * Literal drop-in for the numba kernel's call signature (solver.py:294-311):
+ * host arrays in, u2[interior] and flags[ceil(N_i/chunk)] out.  Uploads,
+ * runs one step and downloads every call (slow by construction; the plan API
+ * above is the fast path).
+ */
+int rbf_step_kernel(const double* u1, double* u2, int64_t N,
+                    const int64_t* interior, const int64_t* rows,
+                    const double* weights, const double* f_int, int64_t N_i,
+                    int32_t n, double dt, int64_t chunk, uint8_t* flags,
+                    int32_t device);
+
+/* Introspection for benchmarks / tests. */
+typedef struct rbf_plan_info {
+  int64_t N, N_i;
+  int32_t n;
+  int32_t device;
+  int32_t resident;        /* 1: whole loop runs on-chip in one CTA */
+  int32_t renumbered;      /* 1: rows/nodes permuted (field order restored on get/set) */
+  int32_t kernel_n;        /* compile-time width of the chosen step kernel (0: generic) */
+  int32_t grid, block;     /* streaming kernel launch geometry */
+  int64_t device_bytes;    /* device memory held by the plan */
+  int64_t bytes_per_step;  /* algorithmic HBM bytes per step: N_i*(12n+24) */
+  int64_t launches;        /* kernel launches issued by this plan so far */
+} rbf_plan_info;
+
+int rbf_plan_get_info(const rbf_plan* plan, rbf_plan_info* info);
+
+/* Time `iters` bare step launches (fixed mode, no residual) with CUDA events
+ * on the plan's stream; returns the mean per-launch duration in seconds.
+ * Used by bench.py for the roofline of the dominant kernel. */
+int rbf_time_step_kernel(rbf_plan* plan, double dt, int32_t iters,
+                         double* seconds_per_launch);
+
+void rbf_plan_destroy(rbf_plan* plan);
+const char* rbf_last_error(void);
+int rbf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBFFD_B200_H */

@@ -1,0 +1,118 @@
+"""ctypes binding of the C ABI in include/rbffd_b200.h (librbffd_b200.so).
+
+There is deliberately no fallback: if the shared library is missing or cannot
+be loaded the import of the solver fails loudly.  Build it with
+``python -c "import __graft_entry__ as g; g.build()"`` or ``make -C
+paper_2107_03632_b200/csrc``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "librbffd_b200.so"
+
+RBF_OK = 0
+RBF_ERR_CUDA = 1
+RBF_ERR_PARAM = 2
+RBF_ERR_INSTABILITY = 4
+RBF_ERR_TIMEOUT = 5
+
+RBF_RENUMBER_MORTON = 0x1
+RBF_NO_RESIDENT = 0x2
+RBF_NO_PDL = 0x4
+
+RBF_MODE_FIXED = 0
+RBF_MODE_STEADY = 1
+
+# every symbol include/rbffd_b200.h declares (checked by tests/test_abi.py)
+EXPORTED = (
+    "rbf_plan_create",
+    "rbf_set_forcing",
+    "rbf_set_field",
+    "rbf_get_field",
+    "rbf_run",
+    "rbf_step",
+    "rbf_step_kernel",
+    "rbf_plan_get_info",
+    "rbf_time_step_kernel",
+    "rbf_plan_destroy",
+    "rbf_last_error",
+    "rbf_version",
+)
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("N", ctypes.c_int64),
+        ("N_i", ctypes.c_int64),
+        ("n", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("resident", ctypes.c_int32),
+        ("renumbered", ctypes.c_int32),
+        ("kernel_n", ctypes.c_int32),
+        ("grid", ctypes.c_int32),
+        ("block", ctypes.c_int32),
+        ("device_bytes", ctypes.c_int64),
+        ("bytes_per_step", ctypes.c_int64),
+        ("launches", ctypes.c_int64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+
+
+def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
+    """Load (once) and type the shared library.  Raises OSError if absent."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise OSError(
+            f"{p} not found: the CUDA library is not built "
+            "(run `make -C paper_2107_03632_b200/csrc` or __graft_entry__.build())"
+        )
+    lib = ctypes.CDLL(str(p))
+    vp, i64, i32, u32, dbl = (
+        ctypes.c_void_p,
+        ctypes.c_int64,
+        ctypes.c_int32,
+        ctypes.c_uint32,
+        ctypes.c_double,
+    )
+    pi64 = ctypes.POINTER(ctypes.c_int64)
+    pi32 = ctypes.POINTER(ctypes.c_int32)
+    pdbl = ctypes.POINTER(ctypes.c_double)
+    sig = {
+        "rbf_plan_create": ([ctypes.POINTER(vp), i64, i64, i32, vp, vp, vp, vp, vp, i32, u32], i32),
+        "rbf_set_forcing": ([vp, vp], i32),
+        "rbf_set_field": ([vp, vp], i32),
+        "rbf_get_field": ([vp, vp], i32),
+        "rbf_run": ([vp, dbl, i64, i32, dbl, i64, i32, pi64, pdbl, pi32, pi64, pdbl], i32),
+        "rbf_step": ([vp, dbl], i32),
+        "rbf_step_kernel": ([vp, vp, i64, vp, vp, vp, vp, i64, i32, dbl, i64, vp, i32], i32),
+        "rbf_plan_get_info": ([vp, ctypes.POINTER(PlanInfo)], i32),
+        "rbf_time_step_kernel": ([vp, dbl, i32, pdbl], i32),
+        "rbf_plan_destroy": ([vp], None),
+        "rbf_last_error": ([], ctypes.c_char_p),
+        "rbf_version": ([], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def last_error(lib: ctypes.CDLL | None = None) -> str:
+    lib = lib or load()
+    msg = lib.rbf_last_error()
+    return msg.decode() if msg else ""

@@ -1,0 +1,709 @@
+// rbffd_b200.cu -- host driver + C ABI (include/rbffd_b200.h) of the B200-native
+// explicit RBF-FD time loop.  Replaces rbffd.solver._step_kernel and the step
+// loop of rbffd.solver.run_time_loop (pkg/src/rbffd/solver.py:168-311).
+//
+// Design (DESIGN.md has the long form):
+//  * plan_create packs the reference's row-major ShapeStore into SELL-32 on the
+//    device (pack_rows_kernel) and renumbers nodes so interior row r updates
+//    node B + r.  The renumbering never touches the per-row j order, so the
+//    arithmetic, and therefore every bit, is unchanged.
+//  * small problems (whole working set <= ~220 KB) run the entire loop inside
+//    one CTA's shared memory (resident_loop_kernel): one launch per run.
+//  * everything else runs one streaming launch per step, captured into CUDA
+//    graphs of kGraphSteps steps and chained with programmatic dependent launch
+//    so step s+1 streams its weights while step s drains.  The non-finite
+//    flag, the residual max and the steady-state decision are fused into the
+//    step (last-CTA ticket), so the host only polls a 64-byte status per chunk.
+#include "../../include/rbffd_b200.h"
+#include "step_kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <parallel/algorithm>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define RBF_CK(call)                                                                         \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(RBF_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+constexpr int kGraphSteps = 64;  // steps per captured graph (even: keeps buffer parity)
+constexpr int kStreamBlock = 256;
+constexpr size_t kResidentSmemMax = 227 * 1024;
+
+using StreamFn = void (*)(rbf::StepArgs, const double*, double*, int);
+using ResidentFn = void (*)(rbf::ResidentArgs);
+
+template <int NJ>
+struct KernelSet {
+  static StreamFn stream() { return rbf::step_stream_kernel<NJ>; }
+  static ResidentFn resident() { return rbf::resident_loop_kernel<NJ>; }
+};
+
+// Support sizes with a fully unrolled instantiation; others use the generic
+// runtime-n kernel (same arithmetic, same order).
+#define RBF_SPECIALISED(X) \
+  X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(12) X(15) X(16) X(20) X(21) X(24) X(28) X(30) X(32) \
+  X(36) X(40) X(42) X(45) X(48) X(56) X(60) X(64)
+
+bool pick_kernels(int n, StreamFn* s, ResidentFn* r, int* kn) {
+  switch (n) {
+#define RBF_CASE(K)                        \
+  case K:                                  \
+    *s = KernelSet<K>::stream();           \
+    *r = KernelSet<K>::resident();         \
+    *kn = K;                               \
+    return true;
+    RBF_SPECIALISED(RBF_CASE)
+#undef RBF_CASE
+    default:
+      *s = KernelSet<0>::stream();
+      *r = KernelSet<0>::resident();
+      *kn = 0;
+      return false;
+  }
+}
+
+uint64_t morton2(uint32_t x, uint32_t y) {
+  auto spread = [](uint64_t v) {
+    v &= 0x1fffffull;
+    v = (v | (v << 32)) & 0x1f00000000ffffull;
+    v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+    v = (v | (v << 8)) & 0x100f00f00f00f00full;
+    v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
+    return v;
+  };
+  return spread(x) | (spread(y) << 1);
+}
+
+}  // namespace
+
+struct rbf_plan {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t N = 0, N_i = 0, B = 0, S = 0;
+  int n = 0;
+  double* W = nullptr;
+  int* C = nullptr;
+  double* F = nullptr;
+  double* U[2] = {nullptr, nullptr};
+  double* tmp = nullptr;      // N doubles for permuted field transfers
+  int* new_id = nullptr;      // [N] original -> plan node id; nullptr = identity
+  long long* row_of_k = nullptr;  // [N_i] reference row k -> plan row; nullptr = identity
+  rbf::DevStatus* st = nullptr;
+  rbf::DevStatus* h_st = nullptr;  // pinned
+  StreamFn stream_fn = nullptr;
+  ResidentFn resident_fn = nullptr;
+  int kernel_n = 0;
+  bool resident = false;
+  size_t resident_smem = 0;
+  bool renumbered = false;
+  bool pdl = true;
+  int grid = 1;
+  int cur = 0;                // buffer holding the current field
+  cudaGraphExec_t graphs[4] = {nullptr, nullptr, nullptr, nullptr};  // [copy_back*2 + steady]
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t launches = 0;
+  int64_t device_bytes = 0;
+
+  rbf::StepArgs args() const {
+    rbf::StepArgs a;
+    a.W = W;
+    a.C = C;
+    a.F = F;
+    a.n_rows = N_i;
+    a.dst_base = B;
+    a.n = n;
+    a.st = st;
+    return a;
+  }
+};
+
+namespace {
+
+template <typename T>
+int dev_alloc(rbf_plan* p, T** ptr, size_t count) {
+  if (count == 0) count = 1;
+  RBF_CK(cudaMalloc(reinterpret_cast<void**>(ptr), count * sizeof(T)));
+  p->device_bytes += static_cast<int64_t>(count * sizeof(T));
+  return RBF_OK;
+}
+
+#define RBF_TRY(expr)          \
+  do {                         \
+    int rc_ = (expr);          \
+    if (rc_ != RBF_OK) return rc_; \
+  } while (0)
+
+// One streaming step: reads U[in], writes U[1-in].
+int launch_step(rbf_plan* p, int in, int flags) {
+  if (p->N_i == 0) return RBF_OK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p->grid);
+  cfg.blockDim = dim3(kStreamBlock);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = p->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = p->pdl ? 1 : 0;
+  RBF_CK(cudaLaunchKernelEx(&cfg, p->stream_fn, p->args(), static_cast<const double*>(p->U[in]),
+                            p->U[1 - in], flags));
+  ++p->launches;
+  return RBF_OK;
+}
+
+// A copy-back step (paper Listing 1, solver.py:213): U[0] -> U[1], then U[0] = U[1].
+int launch_copy_back_step(rbf_plan* p, int flags) {
+  RBF_TRY(launch_step(p, 0, flags));
+  RBF_CK(cudaMemcpyAsync(p->U[0], p->U[1], sizeof(double) * p->N, cudaMemcpyDeviceToDevice,
+                         p->stream));
+  return RBF_OK;
+}
+
+int get_graph(rbf_plan* p, bool copy_back, bool steady, cudaGraphExec_t* out) {
+  const int slot = (copy_back ? 2 : 0) + (steady ? 1 : 0);
+  if (p->graphs[slot]) {
+    *out = p->graphs[slot];
+    return RBF_OK;
+  }
+  const int flags = steady ? (rbf::kNeedResidual | rbf::kSteady) : 0;
+  RBF_CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = RBF_OK;
+  const int64_t before = p->launches;
+  for (int i = 0; i < kGraphSteps && rc == RBF_OK; ++i)
+    rc = copy_back ? launch_copy_back_step(p, flags) : launch_step(p, i & 1, flags);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(p->stream, &g);
+  p->launches = before;  // captured launches are counted when the graph runs
+  if (rc != RBF_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) return fail(RBF_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  cudaGraphExec_t ge = nullptr;
+  e = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(RBF_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  p->graphs[slot] = ge;
+  *out = ge;
+  return RBF_OK;
+}
+
+int reset_status(rbf_plan* p, double dt, double tol) {
+  rbf::DevStatus s = {};
+  s.res_bits = 0;
+  s.last_res_bits = 0;
+  s.last_res_step = -1;
+  s.bad_step = -1;
+  s.conv_step = -1;
+  s.step = 0;
+  s.ticket = 0;
+  s.dt = dt;
+  s.tol = tol;
+  *p->h_st = s;
+  RBF_CK(cudaMemcpyAsync(p->st, p->h_st, sizeof(s), cudaMemcpyHostToDevice, p->stream));
+  return RBF_OK;
+}
+
+int read_status(rbf_plan* p) {
+  RBF_CK(cudaMemcpyAsync(p->h_st, p->st, sizeof(rbf::DevStatus), cudaMemcpyDeviceToHost, p->stream));
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  return RBF_OK;
+}
+
+// Make U[0] hold the current field so graph parity (step s reads U[s % 2]) holds.
+int normalise_current(rbf_plan* p) {
+  if (p->cur != 0) {
+    RBF_CK(cudaMemcpyAsync(p->U[0], p->U[1], sizeof(double) * p->N, cudaMemcpyDeviceToDevice,
+                           p->stream));
+    p->cur = 0;
+  }
+  return RBF_OK;
+}
+
+int run_streaming(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
+  const int step_flags = steady ? (rbf::kNeedResidual | rbf::kSteady) : 0;
+  cudaGraphExec_t graph = nullptr;
+  if (limit > kGraphSteps) RBF_TRY(get_graph(p, copy_back, steady, &graph));
+  RBF_CK(cudaEventRecord(p->ev0, p->stream));
+  int64_t launched = 0;
+  if (!steady) {
+    const int64_t chunks = (limit - 1) / kGraphSteps;
+    for (int64_t c = 0; c < chunks; ++c) {
+      RBF_CK(cudaGraphLaunch(graph, p->stream));
+      p->launches += kGraphSteps;
+    }
+    launched = chunks * kGraphSteps;
+    for (; launched < limit; ++launched) {
+      const int fl = (launched == limit - 1) ? rbf::kNeedResidual : 0;
+      if (copy_back) RBF_TRY(launch_copy_back_step(p, fl));
+      else RBF_TRY(launch_step(p, static_cast<int>(launched & 1), fl));
+    }
+    RBF_CK(cudaEventRecord(p->ev1, p->stream));
+    return RBF_OK;
+  }
+  // Steady: poll the device status once per chunk, keeping two chunks in
+  // flight; steps issued after convergence are no-ops on the device.
+  int in_flight = 0;
+  cudaEvent_t evs[2];
+  RBF_CK(cudaEventCreateWithFlags(&evs[0], cudaEventDisableTiming));
+  RBF_CK(cudaEventCreateWithFlags(&evs[1], cudaEventDisableTiming));
+  int which = 0;
+  int rc = RBF_OK;
+  while (launched < limit && rc == RBF_OK) {
+    if (graph && limit - launched >= kGraphSteps) {
+      if (cudaGraphLaunch(graph, p->stream) != cudaSuccess) { rc = fail(RBF_ERR_CUDA, "graph launch"); break; }
+      p->launches += kGraphSteps;
+      launched += kGraphSteps;
+    } else {
+      for (; launched < limit && rc == RBF_OK; ++launched)
+        rc = copy_back ? launch_copy_back_step(p, step_flags)
+                       : launch_step(p, static_cast<int>(launched & 1), step_flags);
+      if (rc != RBF_OK) break;
+    }
+    cudaEventRecord(evs[which], p->stream);
+    ++in_flight;
+    which ^= 1;
+    if (in_flight == 2 && launched < limit) {
+      // wait for the older chunk, then peek at the status
+      cudaEventSynchronize(evs[which]);
+      --in_flight;
+      rbf::DevStatus s;
+      if (cudaMemcpy(&s, p->st, sizeof(s), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        rc = fail(RBF_ERR_CUDA, "status poll");
+        break;
+      }
+      if (s.bad_step >= 0 || s.conv_step >= 0) break;
+    }
+  }
+  cudaEventRecord(p->ev1, p->stream);
+  cudaStreamSynchronize(p->stream);
+  cudaEventDestroy(evs[0]);
+  cudaEventDestroy(evs[1]);
+  return rc;
+}
+
+int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
+  RBF_CK(cudaEventRecord(p->ev0, p->stream));
+  if (limit > 0 && p->N_i > 0) {
+    rbf::ResidentArgs a;
+    a.W = p->W;
+    a.C = p->C;
+    a.F = p->F;
+    a.U0 = p->U[0];
+    a.U1 = p->U[1];
+    a.n_rows = p->N_i;
+    a.N = p->N;
+    a.dst_base = p->B;
+    a.limit = limit;
+    a.n = p->n;
+    a.flags = steady ? rbf::kSteady : 0;
+    a.copy_back = copy_back ? 1 : 0;
+    a.st = p->st;
+    const int threads = static_cast<int>(std::min<int64_t>(1024, ((p->N_i + 31) / 32) * 32));
+    p->resident_fn<<<1, threads, p->resident_smem, p->stream>>>(a);
+    RBF_CK(cudaGetLastError());
+    ++p->launches;
+  }
+  RBF_CK(cudaEventRecord(p->ev1, p->stream));
+  return RBF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rbf_version(void) { return 1; }
+
+const char* rbf_last_error(void) { return g_err.c_str(); }
+
+int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int64_t* interior,
+                    const int64_t* rows, const double* weights, const double* f_int,
+                    const double* positions, int32_t device, uint32_t flags) {
+  if (!out) return fail(RBF_ERR_PARAM, "out is NULL");
+  *out = nullptr;
+  if (N < 1 || N > std::numeric_limits<int32_t>::max())
+    return fail(RBF_ERR_PARAM, "N must be in [1, 2^31-1]");
+  if (N_i < 0 || N_i > N) return fail(RBF_ERR_PARAM, "need 0 <= N_i <= N");
+  if (n < 1) return fail(RBF_ERR_PARAM, "support size n must be >= 1");
+  if (N_i > 0 && (!interior || !rows || !weights || !f_int))
+    return fail(RBF_ERR_PARAM, "interior/rows/weights/f_int must be non-NULL");
+  const bool morton = (flags & RBF_RENUMBER_MORTON) != 0;
+  if (morton && !positions) return fail(RBF_ERR_PARAM, "RBF_RENUMBER_MORTON needs positions");
+
+  // ---- host-side validation + renumbering ----------------------------------
+  const int64_t B = N - N_i;
+  std::vector<uint8_t> seen(static_cast<size_t>(N), 0);
+  bool identity = !morton;
+  for (int64_t k = 0; k < N_i; ++k) {
+    const int64_t v = interior[k];
+    if (v < 0 || v >= N) return fail(RBF_ERR_PARAM, "interior node id out of range");
+    if (seen[v]) return fail(RBF_ERR_PARAM, "interior node ids must be distinct");
+    seen[v] = 1;
+    if (v != B + k) identity = false;
+  }
+  std::vector<int64_t> row_of_k;  // k -> plan row (empty: identity)
+  std::vector<int32_t> new_id;    // original node -> plan node (empty: identity)
+  if (!identity) {
+    std::vector<int64_t> order(static_cast<size_t>(N_i));
+    for (int64_t k = 0; k < N_i; ++k) order[k] = k;
+    if (morton && N_i > 1) {
+      double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
+      for (int64_t i = 0; i < N; ++i) {
+        xmin = std::min(xmin, positions[2 * i]);
+        xmax = std::max(xmax, positions[2 * i]);
+        ymin = std::min(ymin, positions[2 * i + 1]);
+        ymax = std::max(ymax, positions[2 * i + 1]);
+      }
+      const double sx = (xmax > xmin) ? 2097151.0 / (xmax - xmin) : 0.0;
+      const double sy = (ymax > ymin) ? 2097151.0 / (ymax - ymin) : 0.0;
+      std::vector<uint64_t> code(static_cast<size_t>(N_i));
+#pragma omp parallel for schedule(static)
+      for (int64_t k = 0; k < N_i; ++k) {
+        const int64_t v = interior[k];
+        const uint32_t qx = static_cast<uint32_t>((positions[2 * v] - xmin) * sx);
+        const uint32_t qy = static_cast<uint32_t>((positions[2 * v + 1] - ymin) * sy);
+        code[k] = morton2(qx, qy);
+      }
+      __gnu_parallel::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+        return code[a] < code[b] || (code[a] == code[b] && a < b);
+      });
+    }
+    row_of_k.resize(static_cast<size_t>(N_i));
+    for (int64_t r = 0; r < N_i; ++r) row_of_k[order[r]] = r;
+    new_id.assign(static_cast<size_t>(N), -1);
+    int32_t next = 0;
+    for (int64_t i = 0; i < N; ++i)
+      if (!seen[i]) new_id[i] = next++;
+    for (int64_t k = 0; k < N_i; ++k) new_id[interior[k]] = static_cast<int32_t>(B + row_of_k[k]);
+  }
+  seen.clear();
+  seen.shrink_to_fit();
+
+  std::unique_ptr<rbf_plan> p(new rbf_plan());
+  p->device = device;
+  p->N = N;
+  p->N_i = N_i;
+  p->B = B;
+  p->n = n;
+  p->S = (N_i + 31) / 32;
+  p->renumbered = !identity;
+  p->pdl = (flags & RBF_NO_PDL) == 0;
+  RBF_CK(cudaSetDevice(device));
+  RBF_CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  RBF_CK(cudaEventCreate(&p->ev0));
+  RBF_CK(cudaEventCreate(&p->ev1));
+  RBF_CK(cudaMallocHost(reinterpret_cast<void**>(&p->h_st), sizeof(rbf::DevStatus)));
+  RBF_TRY(dev_alloc(p.get(), &p->st, 1));
+  const size_t sell = static_cast<size_t>(p->S) * 32 * n;
+  RBF_TRY(dev_alloc(p.get(), &p->W, sell));
+  RBF_TRY(dev_alloc(p.get(), &p->C, sell));
+  RBF_TRY(dev_alloc(p.get(), &p->F, static_cast<size_t>(p->S) * 32));
+  RBF_TRY(dev_alloc(p.get(), &p->U[0], static_cast<size_t>(N)));
+  RBF_TRY(dev_alloc(p.get(), &p->U[1], static_cast<size_t>(N)));
+  RBF_CK(cudaMemsetAsync(p->W, 0, sell * sizeof(double), p->stream));
+  RBF_CK(cudaMemsetAsync(p->C, 0, sell * sizeof(int), p->stream));
+  RBF_CK(cudaMemsetAsync(p->F, 0, static_cast<size_t>(p->S) * 32 * sizeof(double), p->stream));
+  RBF_CK(cudaMemsetAsync(p->U[0], 0, static_cast<size_t>(N) * sizeof(double), p->stream));
+  RBF_CK(cudaMemsetAsync(p->U[1], 0, static_cast<size_t>(N) * sizeof(double), p->stream));
+
+  // ---- device-side SELL-32 packing, in row chunks ---------------------------
+  long long* d_row_of_k = nullptr;
+  if (!identity) {
+    RBF_TRY(dev_alloc(p.get(), &p->new_id, static_cast<size_t>(N)));
+    RBF_TRY(dev_alloc(p.get(), &p->tmp, static_cast<size_t>(N)));
+    RBF_CK(cudaMemcpy(p->new_id, new_id.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+    if (N_i > 0) {
+      RBF_TRY(dev_alloc(p.get(), &p->row_of_k, static_cast<size_t>(N_i)));
+      d_row_of_k = p->row_of_k;
+      RBF_CK(cudaMemcpy(d_row_of_k, row_of_k.data(), sizeof(long long) * N_i, cudaMemcpyHostToDevice));
+    }
+  }
+  int* d_err = nullptr;
+  RBF_CK(cudaMalloc(&d_err, sizeof(int)));
+  RBF_CK(cudaMemset(d_err, 0, sizeof(int)));
+  if (N_i > 0) {
+    const int64_t chunk_rows = std::max<int64_t>(1, (int64_t(1) << 25) / n);
+    const int64_t cap = std::min<int64_t>(chunk_rows, N_i);
+    double* d_w = nullptr;
+    long long* d_c = nullptr;
+    double* d_f = nullptr;
+    RBF_CK(cudaMalloc(&d_w, sizeof(double) * cap * n));
+    RBF_CK(cudaMalloc(&d_c, sizeof(long long) * cap * n));
+    RBF_CK(cudaMalloc(&d_f, sizeof(double) * cap));
+    for (int64_t k0 = 0; k0 < N_i; k0 += cap) {
+      const int64_t cnt = std::min<int64_t>(cap, N_i - k0);
+      RBF_CK(cudaMemcpyAsync(d_w, weights + k0 * n, sizeof(double) * cnt * n, cudaMemcpyHostToDevice, p->stream));
+      RBF_CK(cudaMemcpyAsync(d_c, rows + k0 * n, sizeof(long long) * cnt * n, cudaMemcpyHostToDevice, p->stream));
+      RBF_CK(cudaMemcpyAsync(d_f, f_int + k0, sizeof(double) * cnt, cudaMemcpyHostToDevice, p->stream));
+      const int64_t total = cnt * n;
+      const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 32));
+      rbf::pack_rows_kernel<<<blocks, 256, 0, p->stream>>>(d_w, d_c, d_f, k0, cnt, n, d_row_of_k,
+                                                           p->new_id, N, p->W, p->C, p->F, d_err);
+      RBF_CK(cudaGetLastError());
+    }
+    RBF_CK(cudaStreamSynchronize(p->stream));
+    cudaFree(d_w);
+    cudaFree(d_c);
+    cudaFree(d_f);
+  }
+  int h_err = 0;
+  RBF_CK(cudaMemcpy(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(d_err);
+  if (h_err) {
+    rbf_plan_destroy(p.release());
+    return fail(RBF_ERR_PARAM, "stencil node id out of range");
+  }
+
+  // ---- kernel selection -----------------------------------------------------
+  pick_kernels(n, &p->stream_fn, &p->resident_fn, &p->kernel_n);
+  const int64_t rows_pad = ((N_i + 31) / 32) * 32;
+  const size_t smem = static_cast<size_t>(rows_pad) * n * (sizeof(double) + sizeof(int)) +
+                      static_cast<size_t>(rows_pad) * sizeof(double) +
+                      2 * static_cast<size_t>(N) * sizeof(double);
+  if (!(flags & RBF_NO_RESIDENT) && N_i > 0 && smem <= kResidentSmemMax - 1024) {
+    if (cudaFuncSetAttribute(p->resident_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) == cudaSuccess) {
+      p->resident = true;
+      p->resident_smem = smem;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  int sms = 148, per_sm = 1;
+  RBF_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p->stream_fn, kStreamBlock, 0));
+  per_sm = std::max(per_sm, 1);
+  const int64_t need = (N_i + kStreamBlock - 1) / kStreamBlock;
+  p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  *out = p.release();
+  return RBF_OK;
+}
+
+int rbf_set_forcing(rbf_plan* p, const double* f_int) {
+  if (!p || (p->N_i > 0 && !f_int)) return fail(RBF_ERR_PARAM, "NULL argument");
+  if (p->N_i == 0) return RBF_OK;
+  RBF_CK(cudaSetDevice(p->device));
+  if (!p->renumbered) {
+    RBF_CK(cudaMemcpyAsync(p->F, f_int, sizeof(double) * p->N_i, cudaMemcpyHostToDevice, p->stream));
+    RBF_CK(cudaStreamSynchronize(p->stream));
+    return RBF_OK;
+  }
+  // Renumbered: F[row_of_k[k]] = f_int[k].
+  RBF_CK(cudaMemcpyAsync(p->tmp, f_int, sizeof(double) * p->N_i, cudaMemcpyHostToDevice, p->stream));
+  const int blocks = static_cast<int>(std::min<int64_t>((p->N_i + 255) / 256, 148 * 16));
+  rbf::scatter_rows_kernel<<<blocks, 256, 0, p->stream>>>(p->tmp, p->row_of_k, p->N_i, p->F);
+  RBF_CK(cudaGetLastError());
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  return RBF_OK;
+}
+
+int rbf_set_field(rbf_plan* p, const double* u) {
+  if (!p || !u) return fail(RBF_ERR_PARAM, "NULL argument");
+  RBF_CK(cudaSetDevice(p->device));
+  const size_t bytes = sizeof(double) * p->N;
+  if (!p->new_id) {
+    RBF_CK(cudaMemcpyAsync(p->U[0], u, bytes, cudaMemcpyHostToDevice, p->stream));
+    RBF_CK(cudaMemcpyAsync(p->U[1], p->U[0], bytes, cudaMemcpyDeviceToDevice, p->stream));
+  } else {
+    RBF_CK(cudaMemcpyAsync(p->tmp, u, bytes, cudaMemcpyHostToDevice, p->stream));
+    const int blocks = static_cast<int>(std::min<int64_t>((p->N + 255) / 256, 148 * 16));
+    rbf::scatter_field_kernel<<<blocks, 256, 0, p->stream>>>(p->tmp, p->new_id, p->N, p->U[0], p->U[1]);
+    RBF_CK(cudaGetLastError());
+  }
+  p->cur = 0;
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  return RBF_OK;
+}
+
+int rbf_get_field(rbf_plan* p, double* u) {
+  if (!p || !u) return fail(RBF_ERR_PARAM, "NULL argument");
+  RBF_CK(cudaSetDevice(p->device));
+  const size_t bytes = sizeof(double) * p->N;
+  if (!p->new_id) {
+    RBF_CK(cudaMemcpyAsync(u, p->U[p->cur], bytes, cudaMemcpyDeviceToHost, p->stream));
+  } else {
+    const int blocks = static_cast<int>(std::min<int64_t>((p->N + 255) / 256, 148 * 16));
+    rbf::gather_field_kernel<<<blocks, 256, 0, p->stream>>>(p->U[p->cur], p->new_id, p->N, p->tmp);
+    RBF_CK(cudaGetLastError());
+    RBF_CK(cudaMemcpyAsync(u, p->tmp, bytes, cudaMemcpyDeviceToHost, p->stream));
+  }
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  return RBF_OK;
+}
+
+int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int64_t max_steps,
+            int32_t copy_back, int64_t* steps_done, double* residual, int32_t* has_residual,
+            int64_t* bad_step, double* device_seconds) {
+  if (!p) return fail(RBF_ERR_PARAM, "plan is NULL");
+  if (mode != RBF_MODE_FIXED && mode != RBF_MODE_STEADY) return fail(RBF_ERR_PARAM, "bad mode");
+  const bool steady = mode == RBF_MODE_STEADY;
+  const int64_t limit = steady ? max_steps : steps;  // solver.py:192
+  if (limit < 0) return fail(RBF_ERR_PARAM, "steps/max_steps must be >= 0");
+  RBF_CK(cudaSetDevice(p->device));
+  RBF_TRY(normalise_current(p));
+  RBF_TRY(reset_status(p, dt, tol));
+  int rc;
+  if (p->resident) rc = run_resident(p, limit, steady, copy_back != 0);
+  else rc = run_streaming(p, limit, steady, copy_back != 0);
+  if (rc != RBF_OK) return rc;
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  RBF_TRY(read_status(p));
+  float ms = 0.f;
+  RBF_CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+  const rbf::DevStatus s = *p->h_st;
+
+  int64_t done = limit > 0 && p->N_i > 0 ? s.step : limit;
+  bool have_res = false;
+  double res = 0.0;
+  if (p->N_i == 0 && limit > 0) {
+    // no interior rows: every step is the identity, residual 0
+    done = steady ? 1 : limit;
+    have_res = true;
+    res = 0.0 / dt;
+  } else if (s.last_res_step >= 0 && s.last_res_step == done - 1) {
+    double m;
+    std::memcpy(&m, &s.last_res_bits, sizeof(m));
+    res = m / dt;  // solver.py:209/:211, same IEEE division as numpy
+    have_res = true;
+  }
+  if (device_seconds) *device_seconds = ms * 1e-3;
+  if (bad_step) *bad_step = s.bad_step;
+  if (s.bad_step >= 0) {
+    // field of the failing step's u2 (solver.py:201)
+    p->cur = copy_back ? 0 : static_cast<int>((s.bad_step + 1) & 1);
+    if (p->resident) p->cur = 0;
+    if (steps_done) *steps_done = s.bad_step;
+    if (has_residual) *has_residual = 0;
+    return fail(RBF_ERR_INSTABILITY, "time loop unstable at step " + std::to_string(s.bad_step));
+  }
+  p->cur = (copy_back || p->resident) ? 0 : static_cast<int>(done & 1);
+  if (steps_done) *steps_done = done;
+  if (residual) *residual = have_res ? res : 0.0;
+  if (has_residual) *has_residual = have_res ? 1 : 0;
+  if (steady && done == max_steps && (!have_res || !(res <= tol))) {
+    return fail(RBF_ERR_TIMEOUT, "no steady state after " + std::to_string(done) + " steps");
+  }
+  return RBF_OK;
+}
+
+int rbf_step(rbf_plan* p, double dt) {
+  if (!p) return fail(RBF_ERR_PARAM, "plan is NULL");
+  RBF_CK(cudaSetDevice(p->device));
+  RBF_TRY(reset_status(p, dt, 0.0));
+  RBF_TRY(launch_step(p, p->cur, 0));
+  RBF_TRY(read_status(p));
+  p->cur ^= 1;
+  if (p->h_st->bad_step >= 0) return fail(RBF_ERR_INSTABILITY, "explicit step produced non-finite values");
+  return RBF_OK;
+}
+
+int rbf_step_kernel(const double* u1, double* u2, int64_t N, const int64_t* interior,
+                    const int64_t* rows, const double* weights, const double* f_int, int64_t N_i,
+                    int32_t n, double dt, int64_t chunk, uint8_t* flags, int32_t device) {
+  if (!u1 || !u2 || (N_i > 0 && !flags)) return fail(RBF_ERR_PARAM, "NULL argument");
+  if (chunk < 1) return fail(RBF_ERR_PARAM, "chunk must be >= 1");
+  rbf_plan* p = nullptr;
+  int rc = rbf_plan_create(&p, N, N_i, n, interior, rows, weights, f_int, nullptr, device,
+                           RBF_NO_RESIDENT);
+  if (rc != RBF_OK) return rc;
+  rc = rbf_set_field(p, u1);
+  if (rc == RBF_OK) {
+    rc = rbf_step(p, dt);
+    if (rc == RBF_ERR_INSTABILITY) rc = RBF_OK;  // reported through flags, like the numba kernel
+  }
+  std::vector<double> out;
+  if (rc == RBF_OK) {
+    out.resize(static_cast<size_t>(N));
+    rc = rbf_get_field(p, out.data());
+  }
+  rbf_plan_destroy(p);
+  if (rc != RBF_OK) return rc;
+  const int64_t n_chunks = std::max<int64_t>(1, (N_i + chunk - 1) / chunk);
+  for (int64_t c = 0; c < n_chunks; ++c) flags[c] = 0;
+  for (int64_t k = 0; k < N_i; ++k) {
+    const double v = out[interior[k]];
+    u2[interior[k]] = v;  // the numba kernel writes u2[interior] only (solver.py:308)
+    if (!std::isfinite(v)) flags[k / chunk] = 1;
+  }
+  return RBF_OK;
+}
+
+int rbf_plan_get_info(const rbf_plan* p, rbf_plan_info* info) {
+  if (!p || !info) return fail(RBF_ERR_PARAM, "NULL argument");
+  info->N = p->N;
+  info->N_i = p->N_i;
+  info->n = p->n;
+  info->device = p->device;
+  info->resident = p->resident ? 1 : 0;
+  info->renumbered = p->renumbered ? 1 : 0;
+  info->kernel_n = p->kernel_n;
+  info->grid = p->grid;
+  info->block = kStreamBlock;
+  info->device_bytes = p->device_bytes;
+  info->bytes_per_step = p->N_i * (12LL * p->n + 24);
+  info->launches = p->launches;
+  return RBF_OK;
+}
+
+int rbf_time_step_kernel(rbf_plan* p, double dt, int32_t iters, double* seconds_per_launch) {
+  if (!p || iters < 1 || !seconds_per_launch) return fail(RBF_ERR_PARAM, "bad argument");
+  RBF_CK(cudaSetDevice(p->device));
+  RBF_TRY(normalise_current(p));
+  RBF_TRY(reset_status(p, dt, 0.0));
+  RBF_CK(cudaEventRecord(p->ev0, p->stream));
+  for (int i = 0; i < iters; ++i) RBF_TRY(launch_step(p, i & 1, 0));
+  RBF_CK(cudaEventRecord(p->ev1, p->stream));
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  float ms = 0.f;
+  RBF_CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+  p->cur = iters & 1;
+  *seconds_per_launch = ms * 1e-3 / iters;
+  return RBF_OK;
+}
+
+void rbf_plan_destroy(rbf_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  for (auto& g : p->graphs)
+    if (g) cudaGraphExecDestroy(g);
+  cudaFree(p->W);
+  cudaFree(p->C);
+  cudaFree(p->F);
+  cudaFree(p->U[0]);
+  cudaFree(p->U[1]);
+  cudaFree(p->tmp);
+  cudaFree(p->new_id);
+  cudaFree(p->row_of_k);
+  cudaFree(p->st);
+  if (p->h_st) cudaFreeHost(p->h_st);
+  if (p->ev0) cudaEventDestroy(p->ev0);
+  if (p->ev1) cudaEventDestroy(p->ev1);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+}
+
+}  // extern "C"

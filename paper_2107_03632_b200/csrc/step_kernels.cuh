@@ -1,0 +1,459 @@
+// step_kernels.cuh -- sm_100a kernels of the explicit RBF-FD pseudo-time step.
+//
+// Reference semantics: rbffd.solver._step_kernel, pkg/src/rbffd/solver.py:294-311
+//   acc = 0.0; for j: acc += weights[k,j]*u1[rows[k,j]]            (:304-306)
+//   value = u1[interior[k]] + dt*(f_int[k] + acc); u2[interior[k]] = value   (:307-308)
+//   flag if !isfinite(value)                                          (:309-311)
+// plus the loop-level pieces of run_time_loop (solver.py:198-217): the per-step
+// non-finite check, the residual max|u2-u1|/dt and the steady-state break, all
+// fused into the step so the host never touches the field between steps.
+//
+// Bitwise parity: numba compiles the update to separate fmul/fadd with no
+// contraction, so every product and sum here is an explicit
+// __dmul_rn / __dadd_rn (ptxas cannot fuse those into DFMA), the accumulator
+// starts at +0.0 and the j-order is serial.
+//
+// Device layout (SELL-32, "sliced transposed ELL"): rows are grouped in
+// slices of 32; slice s stores its n weights as W[s*n*32 + j*32 + lane]
+// (fp64) and node ids as C[...] (int32), so warp-wide loads of one j are one
+// contiguous 256 B (W) / 128 B (C) segment.  Node ids are renumbered so that
+// interior row r updates node (B + r), B = N - N_i (non-interior nodes first),
+// which removes the `interior` array from the stream.  Per-row algorithmic
+// bytes: 8n (W) + 4n (C) + 8 (F) + 8 (u_self) + 8 (u write) = 12n + 24.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rbf {
+
+// Device-resident loop state.  Written only by the last CTA of each step
+// (ticket pattern) or by CTAs that see a non-finite value.
+struct DevStatus {
+  unsigned long long res_bits;       // running max of |u2-u1| bits (>= 0 doubles order like uints)
+  unsigned long long last_res_bits;  // residual numerator of the last residual step
+  long long last_res_step;           // step index of last_res_bits (-1 none)
+  long long bad_step;                // first step with a non-finite value (-1 none)
+  long long conv_step;               // steady: step whose residual <= tol (-1 none)
+  long long step;                    // global index of the next step to execute
+  unsigned int ticket;               // CTAs finished in the current step
+  unsigned int pad0;
+  double dt;
+  double tol;
+};
+
+struct StepArgs {
+  const double* __restrict__ W;  // [S*n*32]
+  const int* __restrict__ C;     // [S*n*32]
+  const double* __restrict__ F;  // [S*32]
+  long long n_rows;
+  long long dst_base;            // node id of row 0 (= N - N_i)
+  int n;
+  DevStatus* st;
+};
+
+enum StepFlags : int {
+  kNeedResidual = 1,  // compute max|u2-u1| for this step
+  kSteady = 2,        // compare residual with tol and set conv_step
+};
+
+// ---- load helpers --------------------------------------------------------
+// Streamed, read-once data (weights, ids, forcing): bypass L1, L2 evict-first,
+// so they do not push the gathered field out of L2.
+__device__ __forceinline__ double ld_stream_f64(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ld_stream_s32(const int* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+               : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// Gathered field values: coherent load (the buffer is written by the previous
+// step, which may still be draining under programmatic dependent launch).
+__device__ __forceinline__ double ld_field(const double* p) { return *p; }
+
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 900)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_launch_dependents() {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 900)
+  asm volatile("griddepcontrol.launch_dependents;");
+#endif
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// One row: serial-j dot product, update, written in exactly the reference
+// association.  `w`/`c` are the row's preloaded weights / node ids.
+template <int NJ>
+__device__ __forceinline__ double row_update(const double (&w)[NJ], const int (&c)[NJ],
+                                             const double* u_in, double f, double u_self,
+                                             double dt) {
+  double g[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) g[j] = ld_field(u_in + c[j]);
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(w[j], g[j]));
+  return __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(f, acc)));
+}
+
+// CTA epilogue shared by the streaming kernels: OR the non-finite flag, max the
+// residual, and let the last CTA of the step finalise the step (ticket).
+__device__ __forceinline__ void step_epilogue(DevStatus* st, long long gstep, bool bad,
+                                              unsigned long long dbits, int flags) {
+  __shared__ unsigned long long s_max[32];
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+  const int any_bad = __syncthreads_or(bad ? 1 : 0);
+  if (any_bad && threadIdx.x == 0) {
+    atomicCAS(reinterpret_cast<unsigned long long*>(&st->bad_step),
+              static_cast<unsigned long long>(-1LL), static_cast<unsigned long long>(gstep));
+  }
+  if (flags & kNeedResidual) {
+    unsigned long long m = warp_max_u64(dbits);
+    if (lane == 0) s_max[warp] = m;
+    __syncthreads();
+    if (warp == 0) {
+      m = lane < nwarps ? s_max[lane] : 0ull;
+      m = warp_max_u64(m);
+      if (lane == 0 && m != 0ull) atomicMax(&st->res_bits, m);
+    }
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int t = atomicAdd(&st->ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    if (flags & kNeedResidual) {
+      const unsigned long long m = atomicExch(&st->res_bits, 0ull);
+      st->last_res_bits = m;
+      st->last_res_step = gstep;
+      if ((flags & kSteady) && st->bad_step < 0) {
+        const double r = __ddiv_rn(__longlong_as_double(static_cast<long long>(m)), st->dt);
+        if (r <= st->tol) st->conv_step = gstep;
+      }
+    }
+    st->ticket = 0u;
+    st->step = gstep + 1;
+    __threadfence();
+  }
+}
+
+// Streaming step: one thread per row, grid-stride over slices.  NJ > 0 is the
+// compile-time support size (fully unrolled); the generic NJ == 0 variant
+// loops over a runtime n.
+template <int NJ>
+__global__ void __launch_bounds__(256)
+step_stream_kernel(StepArgs a, const double* u_in, double* u_out, int flags) {
+  const uint64_t pol = policy_evict_first();
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int n = NJ > 0 ? NJ : a.n;
+  // Let the next step's CTAs get scheduled as ours retire (they still wait in
+  // pdl_wait() before touching the field).
+  pdl_launch_dependents();
+
+  // Prefetch this thread's first row of weights / ids before waiting on the
+  // previous step: they do not depend on it.
+  constexpr int KW = NJ > 0 ? NJ : 1;
+  double w[KW];
+  int c[KW];
+  double f = 0.0;
+  if (NJ > 0 && r < a.n_rows) {
+    const long long base = (r >> 5) * static_cast<long long>(n) * 32 + (r & 31);
+#pragma unroll
+    for (int j = 0; j < KW; ++j) {
+      w[j] = ld_stream_f64(a.W + base + 32LL * j, pol);
+      c[j] = ld_stream_s32(a.C + base + 32LL * j, pol);
+    }
+    f = ld_stream_f64(a.F + r, pol);
+  }
+  pdl_wait();
+
+  DevStatus* st = a.st;
+  const long long gstep = *reinterpret_cast<volatile long long*>(&st->step);
+  const long long bs = *reinterpret_cast<volatile long long*>(&st->bad_step);
+  const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
+  if ((bs >= 0 && bs < gstep) || (cs >= 0 && cs < gstep)) return;  // loop already stopped
+  const double dt = st->dt;
+
+  bool bad = false;
+  unsigned long long dmax = 0ull;
+  bool first = true;
+  for (; r < a.n_rows; r += stride) {
+    const long long node = a.dst_base + r;
+    double value, u_self;
+    if constexpr (NJ > 0) {
+      if (!first) {
+        const long long base = (r >> 5) * static_cast<long long>(n) * 32 + (r & 31);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          w[j] = ld_stream_f64(a.W + base + 32LL * j, pol);
+          c[j] = ld_stream_s32(a.C + base + 32LL * j, pol);
+        }
+        f = ld_stream_f64(a.F + r, pol);
+      }
+      u_self = ld_field(u_in + node);
+      value = row_update<NJ>(w, c, u_in, f, u_self, dt);
+    } else {
+      const long long base = (r >> 5) * static_cast<long long>(n) * 32 + (r & 31);
+      double acc = 0.0;
+      int j = 0;
+      for (; j + 4 <= n; j += 4) {
+        double wv[4], g[4];
+        int cv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          wv[q] = ld_stream_f64(a.W + base + 32LL * (j + q), pol);
+          cv[q] = ld_stream_s32(a.C + base + 32LL * (j + q), pol);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) g[q] = ld_field(u_in + cv[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc = __dadd_rn(acc, __dmul_rn(wv[q], g[q]));
+      }
+      for (; j < n; ++j) {
+        const double wv = ld_stream_f64(a.W + base + 32LL * j, pol);
+        const int cv = ld_stream_s32(a.C + base + 32LL * j, pol);
+        acc = __dadd_rn(acc, __dmul_rn(wv, ld_field(u_in + cv)));
+      }
+      f = ld_stream_f64(a.F + r, pol);
+      u_self = ld_field(u_in + node);
+      value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(f, acc)));
+    }
+    first = false;
+    u_out[node] = value;
+    if (!isfinite(value)) bad = true;
+    if (flags & kNeedResidual) {
+      const double d = fabs(__dsub_rn(value, u_self));
+      const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
+      dmax = b > dmax ? b : dmax;
+    }
+  }
+  step_epilogue(st, gstep, bad, dmax, flags);
+}
+
+// ---------------------------------------------------------------------------
+// Resident loop: the whole problem (weights, ids, forcing, both field buffers)
+// lives in one CTA's shared memory and the CTA runs every step of the loop
+// on-chip.  Used when the working set fits (the paper's Fig. 1 case, N=1025,
+// n=15: ~190 KB), where a launch per step would dominate (the
+// N=1027 case is launch/latency bound).
+struct ResidentArgs {
+  const double* W;   // SELL-32 global copy (read once)
+  const int* C;
+  const double* F;
+  double* U0;        // global field buffers; U0 holds the start field
+  double* U1;
+  long long n_rows;
+  long long N;
+  long long dst_base;
+  long long limit;   // steps to run (fixed: steps, steady: max_steps)
+  int n;
+  int flags;         // kSteady
+  int copy_back;
+  DevStatus* st;
+};
+
+template <int NJ>
+__global__ void __launch_bounds__(1024, 1) resident_loop_kernel(ResidentArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = NJ > 0 ? NJ : a.n;
+  const int rows = static_cast<int>(a.n_rows);
+  const int rows_pad = (rows + 31) & ~31;
+  const int N = static_cast<int>(a.N);
+  // smem: W[n][rows_pad] f64 | F[rows_pad] f64 | U[2][N] f64 | C[n][rows_pad] s32
+  double* sW = reinterpret_cast<double*>(smem_raw);
+  double* sF = sW + static_cast<size_t>(n) * rows_pad;
+  double* sU0 = sF + rows_pad;
+  double* sU1 = sU0 + N;
+  int* sC = reinterpret_cast<int*>(sU1 + N);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ unsigned long long s_red[32];
+  __shared__ int s_stop;
+
+  // Load: SELL-32 (slice-major) -> j-major across the whole CTA.
+  for (int r = tid; r < rows; r += nt) {
+    const long long base = (r >> 5) * static_cast<long long>(n) * 32 + (r & 31);
+    for (int j = 0; j < n; ++j) {
+      sW[j * rows_pad + r] = a.W[base + 32LL * j];
+      sC[j * rows_pad + r] = a.C[base + 32LL * j];
+    }
+    sF[r] = a.F[r];
+  }
+  for (int i = tid; i < N; i += nt) {
+    const double v = a.U0[i];
+    sU0[i] = v;
+    sU1[i] = v;
+  }
+  __syncthreads();
+
+  DevStatus* st = a.st;
+  const double dt = st->dt, tol = st->tol;
+  const bool steady = (a.flags & kSteady) != 0;
+  double* cur = sU0;
+  double* nxt = sU1;
+  long long step = 0;
+  long long bad_step = -1, conv_step = -1;
+  unsigned long long last_bits = 0;
+  long long last_res_step = -1;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+  for (; step < a.limit; ++step) {
+    const bool need_res = steady || (step == a.limit - 1);
+    bool bad = false;
+    unsigned long long dmax = 0ull;
+    for (int r = tid; r < rows; r += nt) {
+      double acc = 0.0;
+      if constexpr (NJ > 0) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+          acc = __dadd_rn(acc, __dmul_rn(sW[j * rows_pad + r], cur[sC[j * rows_pad + r]]));
+      } else {
+        for (int j = 0; j < n; ++j)
+          acc = __dadd_rn(acc, __dmul_rn(sW[j * rows_pad + r], cur[sC[j * rows_pad + r]]));
+      }
+      const int node = static_cast<int>(a.dst_base) + r;
+      const double u_self = cur[node];
+      const double value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(sF[r], acc)));
+      nxt[node] = value;
+      bad |= !isfinite(value);
+      if (need_res) {
+        const unsigned long long b =
+            static_cast<unsigned long long>(__double_as_longlong(fabs(__dsub_rn(value, u_self))));
+        dmax = b > dmax ? b : dmax;
+      }
+    }
+    const int any_bad = __syncthreads_or(bad ? 1 : 0);  // also orders the nxt writes
+    if (any_bad) {
+      bad_step = step;
+      break;  // uniform
+    }
+    if (need_res) {
+      unsigned long long m = warp_max_u64(dmax);
+      if (lane == 0) s_red[warp] = m;
+      __syncthreads();
+      if (warp == 0) {
+        m = lane < nwarps ? s_red[lane] : 0ull;
+        m = warp_max_u64(m);
+        if (lane == 0) {
+          s_red[0] = m;
+          s_stop = steady && (__ddiv_rn(__longlong_as_double(static_cast<long long>(m)), dt) <= tol);
+        }
+      }
+      __syncthreads();
+      last_bits = s_red[0];
+      last_res_step = step;
+      const int stop = s_stop;
+      __syncthreads();  // s_red / s_stop reused next step
+      if (a.copy_back) {
+        for (int i = tid; i < N; i += nt) cur[i] = nxt[i];
+        __syncthreads();
+      } else {
+        double* t = cur; cur = nxt; nxt = t;
+      }
+      if (stop) {
+        conv_step = step;
+        ++step;
+        break;
+      }
+    } else {
+      if (a.copy_back) {
+        for (int i = tid; i < N; i += nt) cur[i] = nxt[i];
+        __syncthreads();
+      } else {
+        double* t = cur; cur = nxt; nxt = t;
+      }
+    }
+  }
+  // Publish: the field the host must read.  After a bad step that is the
+  // failing step's u2 (`nxt`, solver.py:201); otherwise the current buffer.
+  const double* out = (bad_step >= 0) ? nxt : cur;
+  for (int i = tid; i < N; i += nt) {
+    const double v = out[i];
+    a.U0[i] = v;
+    a.U1[i] = v;
+  }
+  if (tid == 0) {
+    st->bad_step = bad_step;
+    st->conv_step = conv_step;
+    st->last_res_bits = last_bits;
+    st->last_res_step = last_res_step;
+    st->step = (bad_step >= 0) ? bad_step + 1 : step;
+  }
+}
+
+// ---- plan construction kernels --------------------------------------------
+// Scatter row-major (reference layout) rows [k0, k0+cnt) into SELL-32 at the
+// renumbered row position; node ids renumbered through new_id.
+__global__ void pack_rows_kernel(const double* __restrict__ w_raw, const long long* __restrict__ c_raw,
+                                 const double* __restrict__ f_raw, long long k0, long long cnt, int n,
+                                 const long long* __restrict__ row_of_k,  // nullptr: identity
+                                 const int* __restrict__ new_id, long long N,
+                                 double* __restrict__ W, int* __restrict__ C, double* __restrict__ F,
+                                 int* __restrict__ err) {
+  const long long total = cnt * n;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long kk = e / n;
+    const int j = static_cast<int>(e - kk * n);
+    const long long k = k0 + kk;
+    const long long r = row_of_k ? row_of_k[k] : k;
+    const long long dst = (r >> 5) * static_cast<long long>(n) * 32 + 32LL * j + (r & 31);
+    const long long col = c_raw[e];
+    if (col < 0 || col >= N) {
+      atomicExch(err, 1);
+      continue;
+    }
+    W[dst] = w_raw[e];
+    C[dst] = new_id ? new_id[col] : static_cast<int>(col);
+    if (j == 0) F[r] = f_raw[kk];
+  }
+}
+
+// u_dev[new_id[i]] = u_host_order[i]   (new_id == nullptr: identity)
+__global__ void scatter_field_kernel(const double* __restrict__ src, const int* __restrict__ new_id,
+                                     long long N, double* __restrict__ d0, double* __restrict__ d1) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < N;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long t = new_id[i];
+    d0[t] = src[i];
+    if (d1) d1[t] = src[i];
+  }
+}
+// F[row_of_k[k]] = f[k]
+__global__ void scatter_rows_kernel(const double* __restrict__ f, const long long* __restrict__ row_of_k,
+                                    long long n_rows, double* __restrict__ F) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n_rows;
+       k += static_cast<long long>(gridDim.x) * blockDim.x)
+    F[row_of_k[k]] = f[k];
+}
+__global__ void gather_field_kernel(const double* __restrict__ src, const int* __restrict__ new_id,
+                                    long long N, double* __restrict__ dst) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < N;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = src[new_id[i]];
+}
+
+}  // namespace rbf

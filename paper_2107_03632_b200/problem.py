@@ -1,0 +1,116 @@
+"""Input containers and manufactured solution of the solve path.
+
+The hot path consumes exactly three objects from the reference's CPU setup:
+``NodeSet`` (pkg/src/rbffd/geometry.py:34-71), ``StencilSet``
+(pkg/src/rbffd/neighborhoods.py:25-35) and ``ShapeStore``
+(pkg/src/rbffd/weights.py:71-86).  The solver here is duck-typed over them:
+the reference's own instances work unchanged; the light-weight mirrors below
+exist so the GPU box (which has no reference package) can hold committed
+fixtures and synthetic domains.
+
+``closed_form_solution`` / ``forcing`` are the same numpy expressions as
+geometry.py:74-86, evaluated in the same order, so they produce the same bits
+(the Dirichlet values and f_int the kernel consumes).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class NodeSet:
+    """Mirror of rbffd.geometry.NodeSet (geometry.py:34-71)."""
+
+    positions: np.ndarray  # (N, 2) float64
+    is_boundary: np.ndarray  # (N,) bool
+    h: float
+
+    @property
+    def n_total(self) -> int:
+        return self.positions.shape[0]
+
+    @property
+    def n_boundary(self) -> int:
+        return int(self.is_boundary.sum())
+
+    @property
+    def n_interior(self) -> int:
+        return self.n_total - self.n_boundary
+
+    @property
+    def interior_indices(self) -> np.ndarray:
+        return np.flatnonzero(~self.is_boundary)
+
+    @property
+    def boundary_indices(self) -> np.ndarray:
+        return np.flatnonzero(self.is_boundary)
+
+
+@dataclass(frozen=True)
+class StencilSet:
+    """Mirror of rbffd.neighborhoods.StencilSet (neighborhoods.py:25-35)."""
+
+    n: int
+    neighbors: np.ndarray  # (N, n) int64, neighbors[i][0] == i
+
+
+@dataclass(frozen=True)
+class ShapeStore:
+    """Mirror of rbffd.weights.ShapeStore (weights.py:71-86).
+
+    ``weights[k]`` applies to ``stencils.neighbors[interior_nodes[k]]``.
+    """
+
+    degree: int
+    interior_nodes: np.ndarray  # (N_i,) int64
+    weights: np.ndarray  # (N_i, n) float64
+    stencils: StencilSet
+
+    @property
+    def n_rows(self) -> int:
+        return self.weights.shape[0]
+
+
+def closed_form_solution(points):
+    """sin(pi x) sin(pi y) -- geometry.py:74-81."""
+    p = np.asarray(points, dtype=float)
+    return np.sin(np.pi * p[..., 0]) * np.sin(np.pi * p[..., 1])
+
+
+def forcing(points):
+    """2 pi^2 sin(pi x) sin(pi y) -- geometry.py:84-86 (same evaluation order)."""
+    return 2.0 * np.pi**2 * closed_form_solution(points)
+
+
+def monomial_count(degree: int) -> int:
+    """MonomialBasis.of_degree(degree).size = (m+1)(m+2)/2 (weights.py:35-68)."""
+    return (degree + 1) * (degree + 2) // 2
+
+
+def node_count_for_spacing(h: float) -> int:
+    """geometry.py:89-95."""
+    return int(math.floor(math.pi / h**2 + 2.0 * math.pi / h + 0.5))
+
+
+def spacing_for_node_count(n: int) -> float:
+    """geometry.py:98-102 (inverse of node_count_for_spacing)."""
+    return 1.0 / (math.sqrt(1.0 + n / math.pi) - 1.0)
+
+
+def load_fixture(path) -> tuple[NodeSet, StencilSet, ShapeStore]:
+    """Rebuild (nodes, stencils, shapes) from a tests/golden/*.npz fixture."""
+    z = np.load(path)
+    nodes = NodeSet(positions=z["positions"], is_boundary=z["is_boundary"], h=float(z["h"]))
+    neighbors = z["neighbors"].astype(np.int64)
+    stencils = StencilSet(n=neighbors.shape[1], neighbors=neighbors)
+    shapes = ShapeStore(
+        degree=int(z["degree"]),
+        interior_nodes=z["interior"].astype(np.int64),
+        weights=z["weights"],
+        stencils=stencils,
+    )
+    return nodes, stencils, shapes

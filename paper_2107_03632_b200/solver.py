@@ -1,0 +1,432 @@
+"""Host-side mirror of rbffd.solver (pkg/src/rbffd/solver.py) over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference:
+
+* ``SolveConfig`` / ``SolveReport``     solver.py:36-119
+* ``apply_dirichlet``                   solver.py:130-138
+* ``explicit_step``                     solver.py:141-165
+* ``run_time_loop``                     solver.py:168-236
+* ``error_norms`` / ``stability_bound`` solver.py:239-254
+* ``save_solution_csv`` / ``save_report_json``  solver.py:262-277
+
+The numba kernel ``_step_kernel`` (solver.py:294-311) and the step loop are
+replaced by the CUDA library (``Plan`` below); the pre/post steps the
+reference does in numpy (Dirichlet values, forcing, auto dt, error norms,
+max|u2| of a failing step) stay on the host with the same expressions, so
+every reported number is bit-identical.  There is no CPU fallback: without
+the built library (or without a CUDA device) these calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import math
+import time
+import weakref
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .errors import DeviceError, InstabilityError, ParameterError, SteadyStateTimeout
+from .problem import closed_form_solution, forcing, monomial_count, spacing_for_node_count
+
+DEFAULT_CHUNK = 1024  # solver.py:30 (CPU chunking knob; GPU geometry is internal)
+_AUTO_DT_SAFETY = 0.5  # solver.py:33
+
+
+@dataclass
+class SolveConfig:
+    """Parameters of one solver run (solver.py:36-96, same validation).
+
+    ``threads`` and ``chunk_size`` are CPU-only knobs of the reference kept for
+    API compatibility; the GPU launch geometry is chosen by the plan.
+    """
+
+    degree: int = 2
+    support_size: int = 15
+    h: Optional[float] = None
+    nodes: Optional[int] = None
+    dt: Optional[float] = None
+    steps: int = 0
+    mode: str = "fixed"
+    tol: float = 1e-9
+    seed: int = 0
+    threads: int = 1
+    chunk_size: int = DEFAULT_CHUNK
+    max_steps: int = 1_000_000
+
+    def __post_init__(self):
+        if self.mode not in ("fixed", "steady"):
+            raise ParameterError(f"mode must be 'fixed' or 'steady', got {self.mode!r}")
+        if (self.h is None) == (self.nodes is None):
+            raise ParameterError("exactly one of h or nodes must be set")
+        if self.dt is not None and not self.dt > 0:
+            raise ParameterError(f"dt must be positive, got {self.dt}")
+        if self.steps < 0:
+            raise ParameterError(f"steps must be >= 0, got {self.steps}")
+        if self.mode == "steady" and not self.tol > 0:
+            raise ParameterError(f"steady tolerance must be positive, got {self.tol}")
+        needed = monomial_count(self.degree) if self.degree >= 0 else None
+        if needed is None:
+            raise ParameterError(f"monomial degree must be >= 0, got {self.degree}")
+        if self.support_size < needed:
+            raise ParameterError(
+                f"support size {self.support_size} below the {needed} "
+                f"monomials of degree {self.degree}"
+            )
+        if self.threads < 1 or self.chunk_size < 1:
+            raise ParameterError("threads and chunk_size must be >= 1")
+
+    def spacing(self) -> float:
+        return self.h if self.h is not None else spacing_for_node_count(self.nodes)
+
+    def as_dict(self, dt_effective: Optional[float] = None) -> dict:
+        return {
+            "m": self.degree,
+            "n": self.support_size,
+            "h": self.h,
+            "nodes": self.nodes,
+            "dt": dt_effective if dt_effective is not None else self.dt,
+            "steps": self.steps,
+            "mode": self.mode,
+            "tol": self.tol,
+            "seed": self.seed,
+            "threads": self.threads,
+            "chunk_size": self.chunk_size,
+        }
+
+
+@dataclass
+class SolveReport:
+    """Outcome of a time loop run (solver.py:99-119).
+
+    ``device_seconds`` (CUDA-event time of the device loop) is extra; it is not
+    part of the JSON schema, which stays the reference's.
+    """
+
+    field: np.ndarray
+    steps: int
+    wall_time_s: float
+    linf: float
+    l2: float
+    residual: Optional[float]
+    config: dict = field(default_factory=dict)
+    device_seconds: Optional[float] = None
+
+    def to_json_dict(self) -> dict:
+        return {
+            "steps": self.steps,
+            "wall_time_s": self.wall_time_s,
+            "linf": self.linf,
+            "l2": self.l2,
+            "residual": self.residual,
+            "config": self.config,
+        }
+
+
+@dataclass
+class RunResult:
+    status: int
+    steps_done: int
+    residual: Optional[float]
+    bad_step: int
+    device_seconds: float
+    wall_seconds: float
+
+
+def _as(a, dtype) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a), dtype=dtype)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+class Plan:
+    """One device-resident problem: packed weights/ids/forcing + both field buffers.
+
+    Wraps ``rbf_plan_create`` .. ``rbf_plan_destroy``.  ``rows`` is the
+    reference's ``neighbors[interior]`` (solver.py:182), row-major.
+    """
+
+    def __init__(self, n_total, interior, rows, weights, f_int, positions=None, *,
+                 renumber: bool = False, device: int = 0, resident: bool = True,
+                 pdl: bool = True):
+        self._lib = _lib.load()
+        interior = _as(interior, np.int64)
+        weights = _as(weights, np.float64)
+        rows = _as(rows, np.int64)
+        f_int = _as(f_int, np.float64)
+        if weights.ndim != 2 or rows.shape != weights.shape:
+            raise ParameterError("rows and weights must both be (N_i, n)")
+        n_rows, n = weights.shape
+        if interior.shape != (n_rows,) or f_int.shape != (n_rows,):
+            raise ParameterError("interior and f_int must have one entry per weight row")
+        flags = 0
+        pos = None
+        if renumber:
+            if positions is None:
+                raise ParameterError("renumbering needs node positions")
+            pos = _as(positions, np.float64)
+            flags |= _lib.RBF_RENUMBER_MORTON
+        if not resident:
+            flags |= _lib.RBF_NO_RESIDENT
+        if not pdl:
+            flags |= _lib.RBF_NO_PDL
+        handle = ctypes.c_void_p()
+        rc = self._lib.rbf_plan_create(
+            ctypes.byref(handle), int(n_total), int(n_rows), int(n), _ptr(interior), _ptr(rows),
+            _ptr(weights), _ptr(f_int), _ptr(pos), int(device), flags,
+        )
+        self._check(rc)
+        self._h = handle
+        self.n_total = int(n_total)
+        self.n_rows = int(n_rows)
+        self.n = int(n)
+        self._finalizer = weakref.finalize(self, self._lib.rbf_plan_destroy, handle)
+
+    # -- plumbing ------------------------------------------------------------
+    def _check(self, rc: int) -> int:
+        if rc == _lib.RBF_OK or rc in (_lib.RBF_ERR_INSTABILITY, _lib.RBF_ERR_TIMEOUT):
+            return rc
+        msg = _lib.last_error(self._lib)
+        if rc == _lib.RBF_ERR_PARAM:
+            raise ParameterError(msg)
+        raise DeviceError(f"CUDA library error {rc}: {msg}")
+
+    def close(self) -> None:
+        self._finalizer()
+
+    def info(self) -> dict:
+        info = _lib.PlanInfo()
+        self._check(self._lib.rbf_plan_get_info(self._h, ctypes.byref(info)))
+        return info.as_dict()
+
+    # -- data ----------------------------------------------------------------
+    def set_forcing(self, f_int) -> None:
+        f_int = _as(f_int, np.float64)
+        if f_int.shape != (self.n_rows,):
+            raise ParameterError("forcing must have one entry per interior row")
+        self._check(self._lib.rbf_set_forcing(self._h, _ptr(f_int)))
+
+    def set_field(self, u) -> None:
+        u = _as(u, np.float64)
+        if u.shape != (self.n_total,):
+            raise ParameterError("field length does not match the node set")
+        self._check(self._lib.rbf_set_field(self._h, _ptr(u)))
+
+    def get_field(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.n_total, dtype=np.float64)
+        self._check(self._lib.rbf_get_field(self._h, _ptr(out)))
+        return out
+
+    # -- compute -------------------------------------------------------------
+    def run(self, dt: float, steps: int = 0, mode: str = "fixed", tol: float = 1e-9,
+            max_steps: int = 1_000_000, copy_back: bool = False) -> RunResult:
+        steps_done = ctypes.c_int64()
+        residual = ctypes.c_double()
+        has_res = ctypes.c_int32()
+        bad = ctypes.c_int64()
+        dev_s = ctypes.c_double()
+        m = _lib.RBF_MODE_STEADY if mode == "steady" else _lib.RBF_MODE_FIXED
+        t0 = time.perf_counter()
+        rc = self._lib.rbf_run(
+            self._h, float(dt), int(steps), m, float(tol), int(max_steps), int(bool(copy_back)),
+            ctypes.byref(steps_done), ctypes.byref(residual), ctypes.byref(has_res),
+            ctypes.byref(bad), ctypes.byref(dev_s),
+        )
+        wall = time.perf_counter() - t0
+        self._check(rc)
+        return RunResult(
+            status=rc,
+            steps_done=steps_done.value,
+            residual=residual.value if has_res.value else None,
+            bad_step=bad.value,
+            device_seconds=dev_s.value,
+            wall_seconds=wall,
+        )
+
+    def step(self, dt: float) -> int:
+        return self._check(self._lib.rbf_step(self._h, float(dt)))
+
+    def time_step_kernel(self, dt: float, iters: int) -> float:
+        out = ctypes.c_double()
+        self._check(self._lib.rbf_time_step_kernel(self._h, float(dt), int(iters), ctypes.byref(out)))
+        return out.value
+
+
+# ---------------------------------------------------------------------------
+# plan cache: one plan per live ShapeStore (explicit_step is called thousands
+# of times on the same shapes in the reference tests, solver tests :231-243)
+_PLANS: dict = {}
+
+
+def _plan_for(shapes, n_total: int, f_int: np.ndarray, positions=None, *, cache: bool = True,
+              renumber: bool = False) -> Plan:
+    weights = shapes.weights
+    neighbors = shapes.stencils.neighbors
+    interior = shapes.interior_nodes
+    key = (id(shapes), weights.ctypes.data, neighbors.ctypes.data, interior.ctypes.data,
+           int(n_total), bool(renumber))
+    if cache:
+        hit = _PLANS.get(key)
+        if hit is not None and hit[0]() is shapes:
+            plan = hit[1]
+            plan.set_forcing(f_int)
+            return plan
+    rows = np.ascontiguousarray(neighbors[interior])  # solver.py:182
+    plan = Plan(n_total, interior, rows, weights, f_int, positions, renumber=renumber)
+    if cache:
+        try:
+            ref = weakref.ref(shapes, lambda _r, k=key: _PLANS.pop(k, None))
+        except TypeError:  # not weak-referenceable: do not cache
+            return plan
+        _PLANS[key] = (ref, plan)
+    return plan
+
+
+def clear_plan_cache() -> None:
+    for _ref, plan in list(_PLANS.values()):
+        plan.close()
+    _PLANS.clear()
+
+
+# ---------------------------------------------------------------------------
+def prepare_problem(config: SolveConfig):
+    """solver.py:122-127.  Setup stays in the reference CPU package (BASELINE
+    north star); this delegates to it when it is importable."""
+    try:
+        from rbffd.solver import prepare_problem as _ref_prepare  # type: ignore
+    except Exception as exc:  # pragma: no cover
+        raise ParameterError(
+            "prepare_problem needs the reference package `rbffd` (node placement, "
+            "kNN and weights stay on the CPU); use paper_2107_03632_b200.synth for "
+            "synthetic domains"
+        ) from exc
+    return _ref_prepare(config)
+
+
+def apply_dirichlet(nodes, values: np.ndarray) -> np.ndarray:
+    """Copy of `values` with boundary entries set to the analytic solution (solver.py:130-138)."""
+    values = np.asarray(values, dtype=float)
+    if values.shape[0] != nodes.n_total:
+        raise ParameterError("field length does not match the node set")
+    out = values.copy()
+    bidx = nodes.boundary_indices
+    out[bidx] = closed_form_solution(nodes.positions[bidx])
+    return out
+
+
+def explicit_step(u1: np.ndarray, shapes, f: np.ndarray, dt: float, *, cache: bool = True) -> np.ndarray:
+    """One explicit update u2 = u1 + dt*(f + L u1) on interior nodes (solver.py:141-165).
+
+    `f` holds per-node forcing (length N); boundary entries are carried over
+    unchanged; `u1` is not modified.  Raises InstabilityError(max_abs=...) on a
+    non-finite update, like the reference.
+    """
+    u1 = np.asarray(u1, dtype=float)
+    interior = shapes.interior_nodes
+    f_int = np.ascontiguousarray(np.asarray(f, dtype=float)[interior])  # solver.py:156
+    plan = _plan_for(shapes, u1.shape[0], f_int, cache=cache)
+    plan.set_field(u1)
+    rc = plan.step(dt)
+    u2 = plan.get_field()
+    if rc == _lib.RBF_ERR_INSTABILITY:
+        max_abs = float(np.max(np.abs(u2)))
+        raise InstabilityError(
+            f"explicit step produced non-finite values (max |u| = {max_abs})",
+            max_abs=max_abs,
+        )
+    return u2
+
+
+def run_time_loop(config: SolveConfig, nodes, shapes, copy_back: bool = False, *,
+                  cache: bool = True, renumber: bool = False) -> SolveReport:
+    """March the explicit iteration on the GPU (solver.py:168-236).
+
+    Starts from zero on the interior and exact Dirichlet values on the
+    boundary; only the step loop is timed (``wall_time_s``).  Keyword-only
+    extras: ``cache`` keeps the packed plan for these shapes alive for the next
+    call; ``renumber`` applies the Morton locality renumbering (bit-identical).
+    """
+    interior = shapes.interior_nodes
+    f_int = np.ascontiguousarray(forcing(nodes.positions[interior]))  # solver.py:184
+    u1 = apply_dirichlet(nodes, np.zeros(nodes.n_total))  # solver.py:186
+    dt = config.dt if config.dt is not None else _AUTO_DT_SAFETY * stability_bound(shapes)
+    plan = _plan_for(shapes, nodes.n_total, f_int, nodes.positions if renumber else None,
+                     cache=cache, renumber=renumber)
+    plan.set_field(u1)
+    res = plan.run(dt, steps=config.steps, mode=config.mode, tol=config.tol,
+                   max_steps=config.max_steps, copy_back=copy_back)
+    if res.status == _lib.RBF_ERR_INSTABILITY:
+        u2 = plan.get_field()
+        max_abs = float(np.max(np.abs(u2)))
+        raise InstabilityError(
+            f"time loop unstable at step {res.bad_step} (max |u| = {max_abs})",
+            step=res.bad_step,
+            max_abs=max_abs,
+        )
+    if res.status == _lib.RBF_ERR_TIMEOUT:
+        raise SteadyStateTimeout(
+            f"no steady state after {res.steps_done} steps (residual {res.residual})",
+            steps=res.steps_done,
+            residual=res.residual,
+        )
+    field_ = plan.get_field()
+    if not cache:
+        plan.close()
+    linf, l2 = error_norms(field_, nodes)
+    return SolveReport(
+        field=field_,
+        steps=res.steps_done,
+        wall_time_s=res.wall_seconds,
+        linf=linf,
+        l2=l2,
+        residual=res.residual,
+        config=config.as_dict(dt_effective=dt),
+        device_seconds=res.device_seconds,
+    )
+
+
+def error_norms(values: np.ndarray, nodes):
+    """(linf, l2) of values minus the analytic solution over all nodes (solver.py:239-246)."""
+    if len(values) != nodes.n_total:
+        raise ParameterError("field length does not match the node set")
+    diff = np.asarray(values, dtype=float) - closed_form_solution(nodes.positions)
+    linf = float(np.max(np.abs(diff)))
+    l2 = float(math.sqrt(float((diff**2).mean())))
+    return linf, l2
+
+
+def stability_bound(shapes) -> float:
+    """2 / max_k sum_j |w_kj| (solver.py:249-254)."""
+    if shapes.n_rows == 0:
+        raise ParameterError("empty shape store")
+    row_sums = np.abs(shapes.weights).sum(axis=1)
+    return float(2.0 / row_sums.max())
+
+
+def effective_threads(requested: int) -> int:
+    """solver.py:257-259 (CPU knob; kept for API compatibility)."""
+    return max(1, int(requested))
+
+
+def save_solution_csv(nodes, values: np.ndarray, path) -> None:
+    """Per-node rows x,y,kind,u,exact,abs_error (solver.py:262-271)."""
+    exact = closed_form_solution(nodes.positions)
+    with open(path, "w", newline="") as fh:
+        fh.write("x,y,kind,u,exact,abs_error\n")
+        for (x, y), b, u, ex in zip(nodes.positions, nodes.is_boundary, values, exact):
+            kind = "boundary" if b else "interior"
+            fh.write(f"{x:.17g},{y:.17g},{kind},{u:.17g},{ex:.17g},{abs(u - ex):.17g}\n")
+
+
+def save_report_json(report: SolveReport, path) -> None:
+    """solver.py:274-277."""
+    with open(path, "w") as fh:
+        json.dump(report.to_json_dict(), fh, indent=2, allow_nan=False)
+        fh.write("\n")

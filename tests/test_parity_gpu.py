@@ -1,0 +1,298 @@
+"""Parity of the CUDA path against the reference's golden vectors and the CPU
+oracle.  Every test runs the sm_100a library through the C ABI; the bar is
+bitwise equality (np.array_equal on fields, == on scalars) -- the reference's
+own tests demand exactly that (test_solver.py:134-145, :189-198).
+
+Mirrors pkg/tests/test_solver.py and acceptance criterion 6; adds the
+device-only variants (streaming vs resident loop, Morton renumbering, graph
+chunking in steady mode) and full-size (BASELINE config 2) parity.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2107_03632_b200 as rb
+from paper_2107_03632_b200 import _lib, synth
+from paper_2107_03632_b200.solver import Plan
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    ("small", "fixed50"),
+    ("small", "fixed120"),
+    ("small", "fixed120_copy"),
+    ("small", "steady"),
+    ("small", "zero"),
+    ("dome", "paper"),
+    ("dome", "steady"),
+    ("crit6", "fixed100"),
+    ("crit6", "fixed100_copy"),
+    ("m4", "fixed200"),
+    ("m6", "fixed100"),
+]
+
+
+def config_for(nodes, shapes, meta, **over):
+    auto = meta["dt"] == 0.5 * rb.stability_bound(shapes)
+    kw = dict(
+        degree=shapes.degree, support_size=shapes.weights.shape[1], nodes=nodes.n_total,
+        dt=None if auto else meta["dt"], steps=meta["config_steps"], mode=meta["mode"],
+        tol=meta["tol"], max_steps=meta["max_steps"],
+    )
+    kw.update(over)
+    return rb.SolveConfig(**kw)
+
+
+def check_report(rep, meta, field):
+    assert np.array_equal(rep.field, field)
+    assert rep.steps == meta["steps"]
+    assert rep.residual == meta["residual"]
+    assert (rep.linf, rep.l2) == (meta["linf"], meta["l2"])
+    assert rep.config["dt"] == meta["dt"]
+
+
+@pytest.mark.parametrize("renumber", [False, True], ids=["native", "morton"])
+@pytest.mark.parametrize("name,case", CASES)
+def test_run_time_loop_matches_reference(golden, manifest, name, case, renumber):
+    nodes, _, shapes, z = golden(name)
+    meta = manifest[name][case]
+    rep = rb.run_time_loop(config_for(nodes, shapes, meta), nodes, shapes,
+                           copy_back=meta["copy_back"], renumber=renumber)
+    check_report(rep, meta, z[f"{case}__field"])
+
+
+@pytest.mark.parametrize("case", ["paper", "steady"])
+def test_streaming_loop_matches_resident_loop(golden, manifest, case):
+    """The Fig. 1 case normally runs on-chip in one CTA; force the streaming
+    graph/PDL path (and its fused steady-state stop) and demand the same bits."""
+    nodes, _, shapes, z = golden("dome")
+    meta = manifest["dome"][case]
+    interior = shapes.interior_nodes
+    rows = shapes.stencils.neighbors[interior]
+    f_int = rb.forcing(nodes.positions[interior])
+    u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    for resident, pdl in ((True, True), (False, True), (False, False)):
+        plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, resident=resident, pdl=pdl)
+        assert plan.info()["resident"] == int(resident)
+        plan.set_field(u0)
+        res = plan.run(meta["dt"], steps=meta["config_steps"], mode=meta["mode"], tol=meta["tol"],
+                       max_steps=meta["max_steps"])
+        assert res.status == _lib.RBF_OK
+        assert res.steps_done == meta["steps"]
+        assert res.residual == meta["residual"]
+        assert np.array_equal(plan.get_field(), z[f"{case}__field"])
+        plan.close()
+
+
+def test_explicit_step_kat_hand_problem(golden):
+    """test_solver.py:112-123."""
+    nodes, _, shapes, z = golden("hand")
+    u1 = z["kat__u1"]
+    f = rb.forcing(nodes.positions)
+    u2 = rb.explicit_step(u1, shapes, f, 3e-3)
+    acc = -11.0 * u1[4] + 2.5 * u1[0] + 2.5 * u1[1] + 3.0 * u1[2] + 3.0 * u1[3]
+    assert u2[4] == pytest.approx(u1[4] + 3e-3 * (f[4] + acc), rel=1e-15)
+    assert np.array_equal(u2, z["kat__u2"])
+    assert np.array_equal(u2[:4], u1[:4])
+
+
+def test_explicit_step_matches_reference_loop(golden):
+    """test_solver.py:134-145 (bitwise vs the numba kernel and the Python loop)."""
+    nodes, stencils, shapes, z = golden("small")
+    u1 = z["step_rand__u1"]
+    snapshot = u1.copy()
+    got = rb.explicit_step(u1, shapes, rb.forcing(nodes.positions), 1e-4)
+    assert np.array_equal(got, z["step_rand__u2"])
+    assert np.array_equal(u1, snapshot)  # test_solver.py:126-131
+
+
+def test_explicit_step_dt_zero_is_identity(golden):
+    nodes, _, shapes, _ = golden("small")
+    u1 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    assert np.array_equal(rb.explicit_step(u1, shapes, rb.forcing(nodes.positions), 0.0), u1)
+
+
+def test_exact_solution_is_near_fixed_point(golden):
+    """test_solver.py:148-159."""
+    nodes, stencils, shapes, _ = golden("small")
+    u_exact = rb.closed_form_solution(nodes.positions)
+    f = rb.forcing(nodes.positions)
+    u2 = rb.explicit_step(u_exact, shapes, f, 1e-5)
+    interior = shapes.interior_nodes
+    residual = f[interior] + np.einsum("ij,ij->i", shapes.weights, u_exact[stencils.neighbors[interior]])
+    assert np.abs(u2 - u_exact).max() <= 1e-5 * np.abs(residual).max() * (1 + 1e-12)
+
+
+def test_explicit_step_detects_blowup(golden, manifest):
+    nodes, _, shapes, _ = golden("small")
+    with pytest.raises(rb.InstabilityError) as ei:
+        rb.explicit_step(np.full(nodes.n_total, 1e308), shapes, rb.forcing(nodes.positions), 1.0)
+    assert ei.value.max_abs is not None
+    assert np.isnan(ei.value.max_abs) == np.isnan(manifest["small"]["step_blowup"]["max_abs"])
+
+
+@pytest.mark.parametrize("name", ["small", "crit6"])
+def test_unstable_dt_raises_at_the_reference_step(golden, manifest, name):
+    """test_solver.py:170-175; the failing step and max|u2| match the oracle."""
+    nodes, _, shapes, _ = golden(name)
+    cfg = rb.SolveConfig(degree=2, support_size=shapes.weights.shape[1], nodes=nodes.n_total,
+                         mode="fixed", steps=500, dt=1.0)
+    want = orc.run_time_loop(nodes, shapes, dt=1.0, steps=500)
+    assert want["status"] == orc.ORC_INSTABILITY
+    if name == "small":
+        assert want["step"] == manifest["small"]["unstable"]["step"]
+    with pytest.raises(rb.InstabilityError) as ei:
+        rb.run_time_loop(cfg, nodes, shapes)
+    assert "step" in str(ei.value)
+    assert ei.value.step == want["step"]
+    assert np.array_equal(np.float64(ei.value.max_abs), np.float64(want["max_abs"]), equal_nan=True)
+
+
+def test_steady_timeout(golden, manifest):
+    nodes, _, shapes, _ = golden("small")
+    cfg = rb.SolveConfig(degree=2, support_size=12, nodes=300, mode="steady", tol=1e-9,
+                         seed=2, max_steps=5)
+    with pytest.raises(rb.SteadyStateTimeout) as ei:
+        rb.run_time_loop(cfg, nodes, shapes)
+    assert ei.value.steps == 5
+    assert ei.value.residual == manifest["small"]["timeout"]["residual"]
+
+
+def test_zero_steps(golden):
+    nodes, _, shapes, _ = golden("small")
+    cfg = rb.SolveConfig(degree=2, support_size=12, nodes=300, steps=0, dt=1e-5)
+    rep = rb.run_time_loop(cfg, nodes, shapes)
+    assert rep.steps == 0 and rep.residual is None
+    assert (rep.linf, rep.l2) == rb.error_norms(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)), nodes)
+
+
+def test_run_time_loop_matches_step_composition(golden):
+    """test_solver.py:189-198."""
+    nodes, _, shapes, _ = golden("small")
+    cfg = rb.SolveConfig(degree=2, support_size=12, nodes=300, steps=50, dt=1e-4)
+    rep = rb.run_time_loop(cfg, nodes, shapes)
+    u = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    f = rb.forcing(nodes.positions)
+    for _ in range(50):
+        u = rb.explicit_step(u, shapes, f, 1e-4)
+    assert np.array_equal(rep.field, u)
+
+
+def test_boundary_held_fixed_and_determinism(golden):
+    """test_solver.py:221-228, :264-273."""
+    nodes, _, shapes, _ = golden("crit6")
+    cfg = rb.SolveConfig(degree=2, support_size=15, nodes=2000, steps=300, dt=1e-5)
+    a = rb.run_time_loop(cfg, nodes, shapes)
+    b = rb.run_time_loop(cfg, nodes, shapes, cache=False)
+    bidx = nodes.boundary_indices
+    assert np.array_equal(a.field[bidx], rb.closed_form_solution(nodes.positions[bidx]))
+    assert np.array_equal(a.field, b.field)
+    assert (a.steps, a.linf, a.l2, a.residual) == (b.steps, b.linf, b.l2, b.residual)
+
+
+def test_residual_monotone_after_startup(golden):
+    """test_solver.py:231-243 through explicit_step on the device."""
+    nodes, _, shapes, _ = golden("small")
+    dt = 0.5 * rb.stability_bound(shapes)
+    u = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    f = rb.forcing(nodes.positions)
+    updates = []
+    for _ in range(3000):
+        new = rb.explicit_step(u, shapes, f, dt)
+        updates.append(np.abs(new - u).max())
+        u = new
+    tail = np.asarray(updates[30:])
+    assert np.all(np.diff(tail) <= 1e-12 * tail[:-1])
+
+
+def test_literal_step_kernel_dropin(golden):
+    """rbf_step_kernel has the numba kernel's signature (solver.py:294-311)."""
+    import ctypes
+
+    nodes, _, shapes, z = golden("crit6")
+    lib = _lib.load()
+    interior = np.ascontiguousarray(shapes.interior_nodes, dtype=np.int64)
+    rows = np.ascontiguousarray(shapes.stencils.neighbors[interior], dtype=np.int64)
+    f_int = np.ascontiguousarray(rb.forcing(nodes.positions[interior]))
+    rng = np.random.default_rng(5)
+    u1 = rb.apply_dirichlet(nodes, rng.normal(size=nodes.n_total))
+    for dt in (1e-5, 1.0e3):
+        u2 = np.full(nodes.n_total, -7.0)
+        want = u2.copy()
+        wflags = orc.step_kernel(u1, want, interior, rows, shapes.weights, f_int, dt, chunk=100)
+        flags = np.zeros_like(wflags)
+        rc = lib.rbf_step_kernel(u1.ctypes.data, u2.ctypes.data, nodes.n_total, interior.ctypes.data,
+                                 rows.ctypes.data, shapes.weights.ctypes.data, f_int.ctypes.data,
+                                 interior.size, rows.shape[1], dt, 100, flags.ctypes.data, 0)
+        assert rc == _lib.RBF_OK
+        assert np.array_equal(u2, want)
+        assert np.array_equal(flags, wflags)
+
+
+def test_no_interior_rows():
+    nodes = rb.NodeSet(positions=np.array([[1.0, 0.0], [0.0, 1.0], [-1.0, 0.0]]),
+                       is_boundary=np.array([True, True, True]), h=0.5)
+    st = rb.StencilSet(n=3, neighbors=np.array([[0, 1, 2], [1, 0, 2], [2, 0, 1]]))
+    shapes = rb.ShapeStore(degree=0, interior_nodes=np.zeros(0, dtype=np.int64),
+                           weights=np.zeros((0, 3)), stencils=st)
+    cfg = rb.SolveConfig(degree=0, support_size=3, nodes=300, steps=3, dt=1e-3)
+    rep = rb.run_time_loop(cfg, nodes, shapes)
+    assert rep.steps == 3 and rep.residual == 0.0
+
+
+# ---- larger synthetic domains: device vs oracle, bitwise ---------------------
+@pytest.fixture(scope="module")
+def synth_cache():
+    return {}
+
+
+def _synth(synth_cache, target, n, m):
+    key = (target, n, m)
+    if key not in synth_cache:
+        synth_cache[key] = synth.synthetic_problem(target, n, m, seed=3)
+    return synth_cache[key]
+
+
+@pytest.mark.parametrize("target,n,m,steps", [
+    (200_000, 15, 2, 40),
+    (100_000, 30, 4, 25),
+    (40_000, 56, 6, 20),
+    (30_000, 19, 2, 33),   # width without a specialised kernel (generic loop)
+])
+@pytest.mark.parametrize("renumber", [False, True], ids=["native", "morton"])
+def test_synthetic_fixed_matches_oracle(synth_cache, target, n, m, steps, renumber):
+    nodes, _, shapes = _synth(synth_cache, target, n, m)
+    want = orc.run_time_loop(nodes, shapes, steps=steps)
+    cfg = rb.SolveConfig(degree=m, support_size=n, nodes=target, steps=steps)
+    rep = rb.run_time_loop(cfg, nodes, shapes, renumber=renumber)
+    assert np.array_equal(rep.field, want["field"])
+    assert rep.residual == want["residual"]
+    assert rep.steps == steps
+
+
+def test_synthetic_steady_streaming_matches_oracle(synth_cache):
+    """Steady mode through the graph-chunked streaming path; the stop step,
+    the residual and the field must equal the oracle's."""
+    nodes, _, shapes = _synth(synth_cache, 30_000, 15, 2)
+    cfg = rb.SolveConfig(degree=2, support_size=15, nodes=30_000, mode="steady", tol=1e-2,
+                         max_steps=200_000)
+    want = orc.run_time_loop(nodes, shapes, mode="steady", tol=1e-2, max_steps=200_000)
+    assert want["status"] == orc.ORC_OK
+    rep = rb.run_time_loop(cfg, nodes, shapes)
+    assert rep.steps == want["steps"]
+    assert rep.residual == want["residual"]
+    assert np.array_equal(rep.field, want["field"])
+
+
+def test_full_size_config2_matches_oracle(synth_cache):
+    """BASELINE config 2 (m=2, n=15, N=1e6) at full size: bitwise vs the oracle
+    over 12 steps, plus swap == copy-back on the device."""
+    nodes, _, shapes = _synth(synth_cache, 1_000_000, 15, 2)
+    want = orc.run_time_loop(nodes, shapes, steps=12)
+    cfg = rb.SolveConfig(degree=2, support_size=15, nodes=1_000_000, steps=12)
+    rep = rb.run_time_loop(cfg, nodes, shapes)
+    assert np.array_equal(rep.field, want["field"])
+    assert rep.residual == want["residual"]
+    cb = rb.run_time_loop(cfg, nodes, shapes, copy_back=True)
+    assert np.array_equal(cb.field, rep.field) and cb.residual == rep.residual
