@@ -223,8 +223,12 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     ap.add_argument("--renumber", action="store_true", help="Morton locality renumbering")
+    ap.add_argument("--ldg", action="store_true", help="plain-load streaming kernel (no TMA ring)")
+    ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--quick", action="store_true",
+                    help="profiling mode: timed region only (no e2e, clock keep-alive, CPU leg)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -258,7 +262,8 @@ def main():
     f_int = np.ascontiguousarray(rb.forcing(nodes.positions[interior]))
     u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
     plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int,
-                nodes.positions if args.renumber else None, renumber=args.renumber, device=local)
+                nodes.positions if args.renumber else None, renumber=args.renumber, device=local,
+                tma=not args.ldg, pdl=not args.no_pdl)
     info = plan.info()
     log(f"plan: {info}")
     plan.set_field(u0)
@@ -273,7 +278,7 @@ def main():
         res = plan.run(dt, steps=args.steps)  # CUDA events on the plan's stream
         torch.cuda.synchronize()
         # keep the GPU busy a little longer so the sampler sees the load
-        if res.device_seconds < 1.0:
+        if res.device_seconds < 1.0 and not args.quick:
             extra = int(min(200_000, max(1, args.steps * (1.0 / max(res.device_seconds, 1e-6)))))
             plan.run(dt, steps=extra)
     gpu_launches = plan.info()["launches"] - launches0  # includes the clock-keepalive run
@@ -292,19 +297,21 @@ def main():
     # ---- end to end through the public API (host arrays in, host field out)
     cfg = rb.SolveConfig(degree=int(shapes.degree), support_size=n, nodes=int(nodes.n_total),
                          dt=dt, steps=args.steps)
-    rb.run_time_loop(cfg, nodes, shapes, cache=False)  # warm (allocator, module load)
-    torch.cuda.synchronize()
-    te = time.perf_counter()
-    rep = rb.run_time_loop(cfg, nodes, shapes, cache=False)
-    torch.cuda.synchronize()
-    t_e2e = time.perf_counter() - te
+    t_e2e = float("nan")
+    if not args.quick:
+        rb.run_time_loop(cfg, nodes, shapes, cache=False)  # warm (allocator, module load)
+        torch.cuda.synchronize()
+        te = time.perf_counter()
+        rb.run_time_loop(cfg, nodes, shapes, cache=False)
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - te
     e2e_value = args.steps * N_i / t_e2e
     h2d = N_i * n * (8 + 8) + N_i * 8 + nodes.n_total * 8  # weights + int64 ids + forcing + field
     d2h = nodes.n_total * 8
     log(f"e2e: {t_e2e * 1e3:.1f} ms -> {e2e_value:.4e} upd/s (plan build + upload + loop + download)")
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if not (args.no_cpu_baseline or args.quick):
         rate, csteps, csec, threads, _ = cpu_baseline(nodes, shapes, dt, args.cpu_budget)
         cpu = {"value": rate, "unit": "node-updates/s", "cores": threads, "kind": "port",
                "sample": f"{csteps} full steps of the same workload ({csec:.1f}s, oracle/ C port "
@@ -331,8 +338,10 @@ def main():
             "l2": (f"inputs larger than L2: {bytes_per_step / 1e6:.0f} MB streamed per step "
                    f"vs 126 MB L2" if bytes_per_step > 126e6 else
                    f"working set {bytes_per_step / 1e6:.1f} MB fits L2 (no flush)"),
-            "loop": "resident on-chip" if info["resident"] else
-                    "streaming step kernel, CUDA graphs of 64 steps + PDL",
+            "loop": {0: "resident on-chip loop (one CTA)",
+                     1: "streaming step (plain loads), CUDA graphs of 64 steps",
+                     2: "streaming step (TMA bulk-copy ring, warp-specialised), CUDA graphs of 64 steps"}[
+                         info["variant"]] + ("" if args.no_pdl or info["resident"] else " + PDL"),
             "parallelism": "single GPU",
         },
         "roofline": {

@@ -23,6 +23,7 @@ RBF_ERR_TIMEOUT = 5
 RBF_RENUMBER_MORTON = 0x1
 RBF_NO_RESIDENT = 0x2
 RBF_NO_PDL = 0x4
+RBF_STREAM_LDG = 0x8
 
 RBF_MODE_FIXED = 0
 RBF_MODE_STEADY = 1
@@ -55,6 +56,7 @@ class PlanInfo(ctypes.Structure):
         ("kernel_n", ctypes.c_int32),
         ("grid", ctypes.c_int32),
         ("block", ctypes.c_int32),
+        ("variant", ctypes.c_int32),
         ("device_bytes", ctypes.c_int64),
         ("bytes_per_step", ctypes.c_int64),
         ("launches", ctypes.c_int64),

@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -50,12 +51,22 @@ constexpr int kStreamBlock = 256;
 constexpr size_t kResidentSmemMax = 227 * 1024;
 
 using StreamFn = void (*)(rbf::StepArgs, const double*, double*, int);
+using TmaFn = void (*)(rbf::StepArgs, const double*, double*, int, rbf::TmaGeom);
 using ResidentFn = void (*)(rbf::ResidentArgs);
 
 template <int NJ>
 struct KernelSet {
   static StreamFn stream() { return rbf::step_stream_kernel<NJ>; }
   static ResidentFn resident() { return rbf::resident_loop_kernel<NJ>; }
+  static TmaFn tma(int cw) {
+    if constexpr (NJ > 0) {
+      return cw >= 16 ? rbf::step_tma_kernel<NJ, 16> : rbf::step_tma_kernel<NJ, 8>;
+    } else {
+      (void)cw;
+      return nullptr;
+    }
+  }
+  static int slice_bytes() { return NJ > 0 ? rbf::tma_slice_bytes<(NJ > 0 ? NJ : 1)>() : 0; }
 };
 
 // Support sizes with a fully unrolled instantiation; others use the generic
@@ -64,12 +75,13 @@ struct KernelSet {
   X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(12) X(15) X(16) X(20) X(21) X(24) X(28) X(30) X(32) \
   X(36) X(40) X(42) X(45) X(48) X(56) X(60) X(64)
 
-bool pick_kernels(int n, StreamFn* s, ResidentFn* r, int* kn) {
+bool pick_kernels(int n, int cw, StreamFn* s, ResidentFn* r, TmaFn* t, int* kn) {
   switch (n) {
 #define RBF_CASE(K)                        \
   case K:                                  \
     *s = KernelSet<K>::stream();           \
     *r = KernelSet<K>::resident();         \
+    *t = KernelSet<K>::tma(cw);            \
     *kn = K;                               \
     return true;
     RBF_SPECIALISED(RBF_CASE)
@@ -77,6 +89,7 @@ bool pick_kernels(int n, StreamFn* s, ResidentFn* r, int* kn) {
     default:
       *s = KernelSet<0>::stream();
       *r = KernelSet<0>::resident();
+      *t = nullptr;
       *kn = 0;
       return false;
   }
@@ -113,6 +126,11 @@ struct rbf_plan {
   rbf::DevStatus* h_st = nullptr;  // pinned
   StreamFn stream_fn = nullptr;
   ResidentFn resident_fn = nullptr;
+  TmaFn tma_fn = nullptr;          // non-null: TMA-pipelined streaming step is used
+  rbf::TmaGeom tma_geom = {1, 2};
+  size_t tma_smem = 0;
+  int tma_block = 0;
+  int variant = 1;                 // 0 resident, 1 LDG streaming, 2 TMA streaming
   int kernel_n = 0;
   bool resident = false;
   size_t resident_smem = 0;
@@ -159,16 +177,21 @@ int launch_step(rbf_plan* p, int in, int flags) {
   if (p->N_i == 0) return RBF_OK;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p->grid);
-  cfg.blockDim = dim3(kStreamBlock);
-  cfg.dynamicSmemBytes = 0;
+  cfg.blockDim = dim3(p->tma_fn ? p->tma_block : kStreamBlock);
+  cfg.dynamicSmemBytes = p->tma_fn ? p->tma_smem : 0;
   cfg.stream = p->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = p->pdl ? 1 : 0;
-  RBF_CK(cudaLaunchKernelEx(&cfg, p->stream_fn, p->args(), static_cast<const double*>(p->U[in]),
-                            p->U[1 - in], flags));
+  if (p->tma_fn) {
+    RBF_CK(cudaLaunchKernelEx(&cfg, p->tma_fn, p->args(), static_cast<const double*>(p->U[in]),
+                              p->U[1 - in], flags, p->tma_geom));
+  } else {
+    RBF_CK(cudaLaunchKernelEx(&cfg, p->stream_fn, p->args(), static_cast<const double*>(p->U[in]),
+                              p->U[1 - in], flags));
+  }
   ++p->launches;
   return RBF_OK;
 }
@@ -477,7 +500,10 @@ int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int
   }
 
   // ---- kernel selection -----------------------------------------------------
-  pick_kernels(n, &p->stream_fn, &p->resident_fn, &p->kernel_n);
+  int cw = 8;
+  if (const char* e = std::getenv("RBFFD_TMA_WARPS")) cw = std::atoi(e) >= 16 ? 16 : 8;
+  TmaFn tma_fn = nullptr;
+  pick_kernels(n, cw, &p->stream_fn, &p->resident_fn, &tma_fn, &p->kernel_n);
   const int64_t rows_pad = ((N_i + 31) / 32) * 32;
   const size_t smem = static_cast<size_t>(rows_pad) * n * (sizeof(double) + sizeof(int)) +
                       static_cast<size_t>(rows_pad) * sizeof(double) +
@@ -493,10 +519,36 @@ int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int
   }
   int sms = 148, per_sm = 1;
   RBF_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p->stream_fn, kStreamBlock, 0));
-  per_sm = std::max(per_sm, 1);
-  const int64_t need = (N_i + kStreamBlock - 1) / kStreamBlock;
-  p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));
+  p->variant = p->resident ? 0 : 1;
+  if (tma_fn && !(flags & RBF_STREAM_LDG) && N_i > 0) {
+    // ring geometry: ~24 KB stages, as many as fit in ~200 KB of shared memory
+    const int slice = n * 32 * 12 + 32 * 8;
+    const int sps = std::max(1, 24576 / slice);
+    const int stage = sps * slice;
+    const int stages = std::max(2, std::min(8, static_cast<int>((200 * 1024) / stage)));
+    const size_t smem_t = 2 * 16 * sizeof(uint64_t) + static_cast<size_t>(stages) * stage;
+    if (smem_t <= kResidentSmemMax &&
+        cudaFuncSetAttribute(tma_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem_t)) == cudaSuccess) {
+      p->tma_fn = tma_fn;
+      p->tma_geom = rbf::TmaGeom{sps, stages};
+      p->tma_smem = smem_t;
+      p->tma_block = 32 * (cw + 1);
+      const int64_t chunks = (p->S + sps - 1) / sps;
+      int occ = 1;
+      RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tma_fn, p->tma_block, smem_t));
+      p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(chunks, int64_t(sms) * std::max(occ, 1))));
+      if (!p->resident) p->variant = 2;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  if (!p->tma_fn) {
+    RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p->stream_fn, kStreamBlock, 0));
+    per_sm = std::max(per_sm, 1);
+    const int64_t need = (N_i + kStreamBlock - 1) / kStreamBlock;
+    p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));
+  }
   RBF_CK(cudaStreamSynchronize(p->stream));
   *out = p.release();
   return RBF_OK;
@@ -661,7 +713,8 @@ int rbf_plan_get_info(const rbf_plan* p, rbf_plan_info* info) {
   info->renumbered = p->renumbered ? 1 : 0;
   info->kernel_n = p->kernel_n;
   info->grid = p->grid;
-  info->block = kStreamBlock;
+  info->block = p->tma_fn ? p->tma_block : kStreamBlock;
+  info->variant = p->variant;
   info->device_bytes = p->device_bytes;
   info->bytes_per_step = p->N_i * (12LL * p->n + 24);
   info->launches = p->launches;

@@ -256,6 +256,180 @@ step_stream_kernel(StepArgs a, const double* u_in, double* u_out, int flags) {
 }
 
 // ---------------------------------------------------------------------------
+// TMA-pipelined streaming step (the default for specialised widths).
+//
+// Warp-specialised and persistent: warp 0 (one elected lane) streams chunks
+// of `sps` SELL slices -- weights, ids and forcing, three contiguous ranges --
+// into a `stages`-deep shared-memory ring with cp.async.bulk (the 1D TMA
+// path) and mbarrier transaction counts; CW consumer warps each take one
+// 32-row slice at a time from the ring, gather u through L1/L2 and write the
+// update.  The copies do not depend on the previous step, so the producer
+// issues the whole ring before griddepcontrol.wait: under programmatic
+// dependent launch step s+1 is already streaming its weights while step s
+// drains.  Arithmetic and j-order are those of row_update (bitwise parity).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+struct TmaGeom {
+  int sps;     // slices per chunk (stage)
+  int stages;  // ring depth
+};
+
+template <int NJ>
+__host__ __device__ constexpr int tma_slice_bytes() {
+  return NJ * 32 * 12 + 32 * 8;
+}
+
+template <int NJ, int CW>
+__global__ void __launch_bounds__(32 * (CW + 1), 1)
+step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeom g) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int kMaxStages = 16;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + kMaxStages;
+  unsigned char* ring = smem_raw + 2 * kMaxStages * sizeof(uint64_t);
+  const int sps = g.sps, stages = g.stages;
+  const int wbytes = sps * NJ * 32 * 8, cbytes = sps * NJ * 32 * 4;
+  const int stage_bytes = sps * tma_slice_bytes<NJ>();
+  const long long S = (a.n_rows + 31) >> 5;
+  const long long nchunks = (S + sps - 1) / sps;
+  const long long my_n = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], static_cast<uint32_t>(sps));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+
+  DevStatus* st = a.st;
+  bool bad = false;
+  unsigned long long dmax = 0ull;
+  long long gstep = 0;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      auto issue = [&](long long i) {
+        const int s = static_cast<int>(i % stages);
+        const long long c = blockIdx.x + i * gridDim.x;
+        const long long s0 = c * sps;
+        const int ns = static_cast<int>(S - s0 < sps ? S - s0 : sps);
+        unsigned char* dst = ring + static_cast<size_t>(s) * stage_bytes;
+        const uint32_t wb = ns * NJ * 32 * 8, cb = ns * NJ * 32 * 4, fb = ns * 32 * 8;
+        mbar_expect_tx(&full[s], wb + cb + fb);
+        bulk_g2s(dst, a.W + s0 * NJ * 32, wb, &full[s], pol);
+        bulk_g2s(dst + wbytes, a.C + s0 * NJ * 32, cb, &full[s], pol);
+        bulk_g2s(dst + wbytes + cbytes, a.F + s0 * 32, fb, &full[s], pol);
+      };
+      const long long pre = my_n < stages ? my_n : stages;
+      for (long long i = 0; i < pre; ++i) issue(i);  // before the dependency wait
+      pdl_wait();
+      const long long g0 = *reinterpret_cast<volatile long long*>(&st->step);
+      const long long bs = *reinterpret_cast<volatile long long*>(&st->bad_step);
+      const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
+      if ((bs >= 0 && bs < g0) || (cs >= 0 && cs < g0)) {
+        for (long long i = 0; i < pre; ++i) mbar_wait(&full[i % stages], 0);  // drain the ring
+        return;
+      }
+      for (long long i = pre; i < my_n; ++i) {
+        const int s = static_cast<int>(i % stages);
+        mbar_wait(&empty[s], static_cast<uint32_t>(((i / stages) - 1) & 1));
+        issue(i);
+      }
+    } else {
+      pdl_wait();
+      const long long g0 = *reinterpret_cast<volatile long long*>(&st->step);
+      const long long bs = *reinterpret_cast<volatile long long*>(&st->bad_step);
+      const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
+      if ((bs >= 0 && bs < g0) || (cs >= 0 && cs < g0)) return;
+    }
+    gstep = *reinterpret_cast<volatile long long*>(&st->step);
+  } else {
+    pdl_wait();
+    gstep = *reinterpret_cast<volatile long long*>(&st->step);
+    const long long bs = *reinterpret_cast<volatile long long*>(&st->bad_step);
+    const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
+    if ((bs >= 0 && bs < gstep) || (cs >= 0 && cs < gstep)) return;
+    const double dt = st->dt;
+    const long long total = my_n * sps;  // slice slots of this CTA
+    for (long long q = warp - 1; q < total; q += CW) {
+      const long long i = q / sps;
+      const int slot = static_cast<int>(q - i * sps);
+      const int s = static_cast<int>(i % stages);
+      mbar_wait(&full[s], static_cast<uint32_t>((i / stages) & 1));
+      const long long slice = (blockIdx.x + i * gridDim.x) * sps + slot;
+      const long long r = slice * 32 + lane;
+      const bool live = slice < S && r < a.n_rows;
+      const unsigned char* base = ring + static_cast<size_t>(s) * stage_bytes;
+      const double* sW = reinterpret_cast<const double*>(base) + slot * NJ * 32;
+      const int* sC = reinterpret_cast<const int*>(base + wbytes) + slot * NJ * 32;
+      const double* sF = reinterpret_cast<const double*>(base + wbytes + cbytes) + slot * 32;
+      if (live) {
+        // ids from the ring -> gathers (all issued before the first use);
+        // weights are read from the ring inside the serial chain
+        double g[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) g[j] = ld_field(u_in + sC[j * 32 + lane]);
+        const long long node = a.dst_base + r;
+        const double u_self = ld_field(u_in + node);
+        const double f = sF[lane];
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(sW[j * 32 + lane], g[j]));
+        const double value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(f, acc)));
+        u_out[node] = value;
+        if (!isfinite(value)) bad = true;
+        if (flags & kNeedResidual) {
+          const unsigned long long b = static_cast<unsigned long long>(
+              __double_as_longlong(fabs(__dsub_rn(value, u_self))));
+          dmax = b > dmax ? b : dmax;
+        }
+      }
+      // slot fully consumed: hand it back to the producer (the arrive has
+      // release semantics; __syncwarp orders the other lanes' shared reads)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+  step_epilogue(st, gstep, bad, dmax, flags);
+}
+
+// ---------------------------------------------------------------------------
 // Resident loop: the whole problem (weights, ids, forcing, both field buffers)
 // lives in one CTA's shared memory and the CTA runs every step of the loop
 // on-chip.  Used when the working set fits (the paper's Fig. 1 case, N=1025,

@@ -72,9 +72,13 @@ def test_streaming_loop_matches_resident_loop(golden, manifest, case):
     rows = shapes.stencils.neighbors[interior]
     f_int = rb.forcing(nodes.positions[interior])
     u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
-    for resident, pdl in ((True, True), (False, True), (False, False)):
-        plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, resident=resident, pdl=pdl)
-        assert plan.info()["resident"] == int(resident)
+    for resident, pdl, tma in ((True, True, True), (False, True, True), (False, False, True),
+                               (False, True, False), (False, False, False)):
+        plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, resident=resident,
+                    pdl=pdl, tma=tma)
+        info = plan.info()
+        assert info["resident"] == int(resident)
+        assert info["variant"] == (0 if resident else (2 if tma else 1))
         plan.set_field(u0)
         res = plan.run(meta["dt"], steps=meta["config_steps"], mode=meta["mode"], tol=meta["tol"],
                        max_steps=meta["max_steps"])
@@ -269,6 +273,26 @@ def test_synthetic_fixed_matches_oracle(synth_cache, target, n, m, steps, renumb
     assert np.array_equal(rep.field, want["field"])
     assert rep.residual == want["residual"]
     assert rep.steps == steps
+
+
+@pytest.mark.parametrize("target,n,m", [(200_000, 15, 2), (60_000, 30, 4), (40_000, 56, 6)])
+def test_tma_and_ldg_step_variants_agree_with_oracle(synth_cache, target, n, m):
+    """Both streaming kernels (TMA ring / plain loads), with and without PDL."""
+    nodes, _, shapes = _synth(synth_cache, target, n, m)
+    interior = shapes.interior_nodes
+    rows = shapes.stencils.neighbors[interior]
+    f_int = rb.forcing(nodes.positions[interior])
+    u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    dt = 0.5 * rb.stability_bound(shapes)
+    want = orc.run_time_loop(nodes, shapes, steps=70)
+    for tma, pdl in ((True, True), (True, False), (False, True)):
+        plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, tma=tma, pdl=pdl)
+        assert plan.info()["variant"] == (2 if tma else 1)
+        plan.set_field(u0)
+        res = plan.run(dt, steps=70)
+        assert res.residual == want["residual"]
+        assert np.array_equal(plan.get_field(), want["field"])
+        plan.close()
 
 
 def test_synthetic_steady_streaming_matches_oracle(synth_cache):
