@@ -58,14 +58,21 @@ template <int NJ>
 struct KernelSet {
   static StreamFn stream() { return rbf::step_stream_kernel<NJ>; }
   static ResidentFn resident() { return rbf::resident_loop_kernel<NJ>; }
-  static TmaFn tma(int cw) {
+  // consumer warps: 15 (512-thread CTA, <=128 regs) for narrow stencils, 8
+  // (<=168 regs) for wide ones whose NJ gathers need the registers
+  static constexpr int kCW = NJ <= 32 ? 15 : 8;
+  static constexpr int kRpl = (NJ > 0 && NJ <= 20) ? 2 : 1;
+  static int cw() { return kCW; }
+  static TmaFn tma(int rpl_req) {
     if constexpr (NJ > 0) {
-      return cw >= 16 ? rbf::step_tma_kernel<NJ, 16> : rbf::step_tma_kernel<NJ, 8>;
+      if (rpl_req == 1 && kRpl != 1) return rbf::step_tma_kernel<NJ, kCW, 1>;
+      return rbf::step_tma_kernel<NJ, kCW, kRpl>;
     } else {
-      (void)cw;
+      (void)rpl_req;
       return nullptr;
     }
   }
+  static int rpl(int rpl_req) { return rpl_req == 1 ? 1 : kRpl; }
   static int slice_bytes() { return NJ > 0 ? rbf::tma_slice_bytes<(NJ > 0 ? NJ : 1)>() : 0; }
 };
 
@@ -75,13 +82,16 @@ struct KernelSet {
   X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(12) X(15) X(16) X(20) X(21) X(24) X(28) X(30) X(32) \
   X(36) X(40) X(42) X(45) X(48) X(56) X(60) X(64)
 
-bool pick_kernels(int n, int cw, StreamFn* s, ResidentFn* r, TmaFn* t, int* kn) {
+bool pick_kernels(int n, int rpl_req, StreamFn* s, ResidentFn* r, TmaFn* t, int* kn, int* rpl,
+                  int* cw) {
   switch (n) {
 #define RBF_CASE(K)                        \
   case K:                                  \
     *s = KernelSet<K>::stream();           \
     *r = KernelSet<K>::resident();         \
-    *t = KernelSet<K>::tma(cw);            \
+    *t = KernelSet<K>::tma(rpl_req);       \
+    *rpl = KernelSet<K>::rpl(rpl_req);     \
+    *cw = KernelSet<K>::cw();              \
     *kn = K;                               \
     return true;
     RBF_SPECIALISED(RBF_CASE)
@@ -91,6 +101,8 @@ bool pick_kernels(int n, int cw, StreamFn* s, ResidentFn* r, TmaFn* t, int* kn) 
       *r = KernelSet<0>::resident();
       *t = nullptr;
       *kn = 0;
+      *rpl = 1;
+      *cw = 8;
       return false;
   }
 }
@@ -500,10 +512,12 @@ int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int
   }
 
   // ---- kernel selection -----------------------------------------------------
-  int cw = 8;
-  if (const char* e = std::getenv("RBFFD_TMA_WARPS")) cw = std::atoi(e) >= 16 ? 16 : 8;
+  int cw = 8;         // consumer warps of the TMA ring kernel (per width, KernelSet::kCW)
+  int rpl_req = 0;    // 0: default rows per lane for the width; 1: force one
+  if (const char* e = std::getenv("RBFFD_TMA_RPL")) rpl_req = std::atoi(e);
   TmaFn tma_fn = nullptr;
-  pick_kernels(n, cw, &p->stream_fn, &p->resident_fn, &tma_fn, &p->kernel_n);
+  int rpl = 1;
+  pick_kernels(n, rpl_req, &p->stream_fn, &p->resident_fn, &tma_fn, &p->kernel_n, &rpl, &cw);
   const int64_t rows_pad = ((N_i + 31) / 32) * 32;
   const size_t smem = static_cast<size_t>(rows_pad) * n * (sizeof(double) + sizeof(int)) +
                       static_cast<size_t>(rows_pad) * sizeof(double) +
@@ -523,9 +537,12 @@ int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int
   if (tma_fn && !(flags & RBF_STREAM_LDG) && N_i > 0) {
     // ring geometry: ~24 KB stages, as many as fit in ~200 KB of shared memory
     const int slice = n * 32 * 12 + 32 * 8;
-    const int sps = std::max(1, 24576 / slice);
+    int sps = std::max(1, 24576 / slice);
+    if (const char* e = std::getenv("RBFFD_TMA_SPS")) sps = std::max(1, std::atoi(e));
+    sps = std::max(rpl, (sps / rpl) * rpl);
     const int stage = sps * slice;
-    const int stages = std::max(2, std::min(8, static_cast<int>((200 * 1024) / stage)));
+    int stages = std::max(2, std::min(8, static_cast<int>((200 * 1024) / stage)));
+    if (const char* e = std::getenv("RBFFD_TMA_STAGES")) stages = std::max(2, std::min(16, std::atoi(e)));
     const size_t smem_t = 2 * 16 * sizeof(uint64_t) + static_cast<size_t>(stages) * stage;
     if (smem_t <= kResidentSmemMax &&
         cudaFuncSetAttribute(tma_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

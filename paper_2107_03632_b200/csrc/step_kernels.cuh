@@ -310,7 +310,9 @@ __host__ __device__ constexpr int tma_slice_bytes() {
   return NJ * 32 * 12 + 32 * 8;
 }
 
-template <int NJ, int CW>
+// RPL: slices per consumer unit (each lane carries RPL independent rows, so a
+// warp keeps RPL*NJ gathers in flight); sps must be a multiple of RPL.
+template <int NJ, int CW, int RPL>
 __global__ void __launch_bounds__(32 * (CW + 1), 1)
 step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeom g) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -318,6 +320,11 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + kMaxStages;
   unsigned char* ring = smem_raw + 2 * kMaxStages * sizeof(uint64_t);
+  // Chunks issued so far by the producer.  A consumer strides CW units ahead
+  // per iteration and can lead the producer by more than one ring lap; an
+  // mbarrier parity wait two phases ahead would alias the previous phase, so
+  // consumers first wait until their chunk has been armed (expect_tx issued).
+  __shared__ int s_issued;
   const int sps = g.sps, stages = g.stages;
   const int wbytes = sps * NJ * 32 * 8, cbytes = sps * NJ * 32 * 4;
   const int stage_bytes = sps * tma_slice_bytes<NJ>();
@@ -327,9 +334,10 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
+    s_issued = 0;
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], static_cast<uint32_t>(sps));
+      mbar_init(&empty[s], static_cast<uint32_t>(sps / RPL));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -355,6 +363,8 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
         bulk_g2s(dst, a.W + s0 * NJ * 32, wb, &full[s], pol);
         bulk_g2s(dst + wbytes, a.C + s0 * NJ * 32, cb, &full[s], pol);
         bulk_g2s(dst + wbytes + cbytes, a.F + s0 * 32, fb, &full[s], pol);
+        __threadfence_block();  // order the arm before the publication below
+        *reinterpret_cast<volatile int*>(&s_issued) = static_cast<int>(i + 1);
       };
       const long long pre = my_n < stages ? my_n : stages;
       for (long long i = 0; i < pre; ++i) issue(i);  // before the dependency wait
@@ -386,41 +396,53 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
     const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
     if ((bs >= 0 && bs < gstep) || (cs >= 0 && cs < gstep)) return;
     const double dt = st->dt;
-    const long long total = my_n * sps;  // slice slots of this CTA
+    const int units_per_chunk = sps / RPL;
+    const long long total = my_n * units_per_chunk;  // consumer units of this CTA
     for (long long q = warp - 1; q < total; q += CW) {
-      const long long i = q / sps;
-      const int slot = static_cast<int>(q - i * sps);
+      const long long i = q / units_per_chunk;
+      const int slot0 = static_cast<int>(q - i * units_per_chunk) * RPL;
       const int s = static_cast<int>(i % stages);
+      if (lane == 0) {
+        while (*reinterpret_cast<volatile int*>(&s_issued) <= i) __nanosleep(64);
+      }
+      __syncwarp();
       mbar_wait(&full[s], static_cast<uint32_t>((i / stages) & 1));
-      const long long slice = (blockIdx.x + i * gridDim.x) * sps + slot;
-      const long long r = slice * 32 + lane;
-      const bool live = slice < S && r < a.n_rows;
       const unsigned char* base = ring + static_cast<size_t>(s) * stage_bytes;
-      const double* sW = reinterpret_cast<const double*>(base) + slot * NJ * 32;
-      const int* sC = reinterpret_cast<const int*>(base + wbytes) + slot * NJ * 32;
-      const double* sF = reinterpret_cast<const double*>(base + wbytes + cbytes) + slot * 32;
-      if (live) {
-        // ids from the ring -> gathers (all issued before the first use);
-        // weights are read from the ring inside the serial chain
-        double g[NJ];
+      const long long slice0 = (blockIdx.x + i * gridDim.x) * sps + slot0;
+      bool live[RPL];
+      double g[RPL][NJ];
+      double u_self[RPL];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) g[j] = ld_field(u_in + sC[j * 32 + lane]);
-        const long long node = a.dst_base + r;
-        const double u_self = ld_field(u_in + node);
-        const double f = sF[lane];
-        double acc = 0.0;
+      for (int t = 0; t < RPL; ++t) {
+        const long long r = (slice0 + t) * 32 + lane;
+        live[t] = (slice0 + t) < S && r < a.n_rows;
+        const int* sC = reinterpret_cast<const int*>(base + wbytes) + (slot0 + t) * NJ * 32;
+        if (live[t]) {
+          // ids from the ring -> gathers, all issued before the first use
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(sW[j * 32 + lane], g[j]));
-        const double value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(f, acc)));
-        u_out[node] = value;
+          for (int j = 0; j < NJ; ++j) g[t][j] = ld_field(u_in + sC[j * 32 + lane]);
+          u_self[t] = ld_field(u_in + a.dst_base + r);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        if (!live[t]) continue;
+        const long long r = (slice0 + t) * 32 + lane;
+        const double* sW = reinterpret_cast<const double*>(base) + (slot0 + t) * NJ * 32;
+        const double* sF = reinterpret_cast<const double*>(base + wbytes + cbytes) + (slot0 + t) * 32;
+        double acc = 0.0;  // weights read from the ring inside the serial chain
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(sW[j * 32 + lane], g[t][j]));
+        const double value = __dadd_rn(u_self[t], __dmul_rn(dt, __dadd_rn(sF[lane], acc)));
+        u_out[a.dst_base + r] = value;
         if (!isfinite(value)) bad = true;
         if (flags & kNeedResidual) {
           const unsigned long long b = static_cast<unsigned long long>(
-              __double_as_longlong(fabs(__dsub_rn(value, u_self))));
+              __double_as_longlong(fabs(__dsub_rn(value, u_self[t]))));
           dmax = b > dmax ? b : dmax;
         }
       }
-      // slot fully consumed: hand it back to the producer (the arrive has
+      // unit fully consumed: hand it back to the producer (the arrive has
       // release semantics; __syncwarp orders the other lanes' shared reads)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);

@@ -295,6 +295,27 @@ def test_tma_and_ldg_step_variants_agree_with_oracle(synth_cache, target, n, m):
         plan.close()
 
 
+@pytest.mark.parametrize("target,n,m", [(1_000_000, 15, 2), (400_000, 30, 4), (200_000, 56, 6)])
+def test_tma_ring_many_laps_matches_ldg(synth_cache, target, n, m):
+    """Hundreds of steps, each wrapping every CTA's ring many times: the TMA
+    ring (producer/consumer mbarrier pipeline) must stay bit-identical to the
+    plain-load kernel (no phase aliasing, no lost or duplicated slices)."""
+    nodes, _, shapes = _synth(synth_cache, target, n, m)
+    interior = shapes.interior_nodes
+    rows = shapes.stencils.neighbors[interior]
+    f_int = rb.forcing(nodes.positions[interior])
+    u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    dt = 0.5 * rb.stability_bound(shapes)
+    out = []
+    for tma in (True, False):
+        plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, tma=tma)
+        plan.set_field(u0)
+        res = plan.run(dt, steps=300)
+        out.append((plan.get_field(), res.residual))
+        plan.close()
+    assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
+
+
 def test_synthetic_steady_streaming_matches_oracle(synth_cache):
     """Steady mode through the graph-chunked streaming path; the stop step,
     the residual and the field must equal the oracle's."""
