@@ -3,7 +3,7 @@
 node-updates/s, and the fraction of the HBM roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c1|c3|c4] [--renumber]
+                    [--workload c2|c1|c3|c4] [--native] [--ldg] [--quick]
 
 One bench "step" is one pseudo-time iteration over every interior row (one
 pass of the hot path, solver.py:198-217); a node-update is one interior row in
@@ -222,7 +222,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
-    ap.add_argument("--renumber", action="store_true", help="Morton locality renumbering")
+    ap.add_argument("--native", action="store_true",
+                    help="keep the native (advancing-front) node order instead of Morton renumbering")
     ap.add_argument("--ldg", action="store_true", help="plain-load streaming kernel (no TMA ring)")
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -261,8 +262,9 @@ def main():
     rows = np.ascontiguousarray(shapes.stencils.neighbors[interior])
     f_int = np.ascontiguousarray(rb.forcing(nodes.positions[interior]))
     u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    renumber = not args.native
     plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int,
-                nodes.positions if args.renumber else None, renumber=args.renumber, device=local,
+                nodes.positions if renumber else None, renumber=renumber, device=local,
                 tma=not args.ldg, pdl=not args.no_pdl)
     info = plan.info()
     log(f"plan: {info}")
@@ -299,10 +301,10 @@ def main():
                          dt=dt, steps=args.steps)
     t_e2e = float("nan")
     if not args.quick:
-        rb.run_time_loop(cfg, nodes, shapes, cache=False)  # warm (allocator, module load)
+        rb.run_time_loop(cfg, nodes, shapes, cache=False, renumber=renumber)  # warm (allocator, module load)
         torch.cuda.synchronize()
         te = time.perf_counter()
-        rb.run_time_loop(cfg, nodes, shapes, cache=False)
+        rb.run_time_loop(cfg, nodes, shapes, cache=False, renumber=renumber)
         torch.cuda.synchronize()
         t_e2e = time.perf_counter() - te
     e2e_value = args.steps * N_i / t_e2e
@@ -334,7 +336,7 @@ def main():
         "config": {
             "workload": WORKLOADS[args.workload][3],
             "N": int(nodes.n_total), "N_i": N_i, "n": n, "m": int(shapes.degree), "dt": dt,
-            "renumber": "morton" if args.renumber else "native (advancing-front order)",
+            "renumber": "morton (bit-identical)" if renumber else "native (advancing-front order)",
             "l2": (f"inputs larger than L2: {bytes_per_step / 1e6:.0f} MB streamed per step "
                    f"vs 126 MB L2" if bytes_per_step > 126e6 else
                    f"working set {bytes_per_step / 1e6:.1f} MB fits L2 (no flush)"),

@@ -61,19 +61,20 @@ struct KernelSet {
   // consumer warps: 15 (512-thread CTA, <=128 regs) for narrow stencils, 8
   // (<=168 regs) for wide ones whose NJ gathers need the registers
   static constexpr int kCW = NJ <= 32 ? 15 : 8;
-  static constexpr int kRpl = (NJ > 0 && NJ <= 20) ? 2 : 1;
-  static int cw() { return kCW; }
   static TmaFn tma(int rpl_req) {
     if constexpr (NJ > 0) {
-      if (rpl_req == 1 && kRpl != 1) return rbf::step_tma_kernel<NJ, kCW, 1>;
-      return rbf::step_tma_kernel<NJ, kCW, kRpl>;
+      // two rows per lane measured slower on B200 (profiles/); opt-in only
+      if constexpr (NJ <= 20) {
+        if (rpl_req == 2) return rbf::step_tma_kernel<NJ, kCW, 2>;
+      }
+      return rbf::step_tma_kernel<NJ, kCW, 1>;
     } else {
       (void)rpl_req;
       return nullptr;
     }
   }
-  static int rpl(int rpl_req) { return rpl_req == 1 ? 1 : kRpl; }
-  static int slice_bytes() { return NJ > 0 ? rbf::tma_slice_bytes<(NJ > 0 ? NJ : 1)>() : 0; }
+  static int rpl(int rpl_req) { return (rpl_req == 2 && NJ > 0 && NJ <= 20) ? 2 : 1; }
+  static int cw() { return kCW; }
 };
 
 // Support sizes with a fully unrolled instantiation; others use the generic
@@ -513,7 +514,7 @@ int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int
 
   // ---- kernel selection -----------------------------------------------------
   int cw = 8;         // consumer warps of the TMA ring kernel (per width, KernelSet::kCW)
-  int rpl_req = 0;    // 0: default rows per lane for the width; 1: force one
+  int rpl_req = 1;    // rows per lane of the TMA consumers (RBFFD_TMA_RPL=2: two, n <= 20)
   if (const char* e = std::getenv("RBFFD_TMA_RPL")) rpl_req = std::atoi(e);
   TmaFn tma_fn = nullptr;
   int rpl = 1;

@@ -346,15 +346,21 @@ def explicit_step(u1: np.ndarray, shapes, f: np.ndarray, dt: float, *, cache: bo
     return u2
 
 
+RENUMBER_MIN_ROWS = 32_768  # auto Morton renumbering from this many interior rows on
+
+
 def run_time_loop(config: SolveConfig, nodes, shapes, copy_back: bool = False, *,
-                  cache: bool = True, renumber: bool = False) -> SolveReport:
+                  cache: bool = True, renumber: Optional[bool] = None) -> SolveReport:
     """March the explicit iteration on the GPU (solver.py:168-236).
 
     Starts from zero on the interior and exact Dirichlet values on the
     boundary; only the step loop is timed (``wall_time_s``).  Keyword-only
     extras: ``cache`` keeps the packed plan for these shapes alive for the next
-    call; ``renumber`` applies the Morton locality renumbering (bit-identical).
+    call; ``renumber`` applies the Morton locality renumbering (bit-identical;
+    default: on from RENUMBER_MIN_ROWS interior rows).
     """
+    if renumber is None:
+        renumber = shapes.n_rows >= RENUMBER_MIN_ROWS
     interior = shapes.interior_nodes
     f_int = np.ascontiguousarray(forcing(nodes.positions[interior]))  # solver.py:184
     u1 = apply_dirichlet(nodes, np.zeros(nodes.n_total))  # solver.py:186
