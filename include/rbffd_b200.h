@@ -147,6 +147,35 @@ int rbf_plan_get_info(const rbf_plan* plan, rbf_plan_info* info);
 int rbf_time_step_kernel(rbf_plan* plan, double dt, int32_t iters,
                          double* seconds_per_launch);
 
+/* ---- node-partitioned multi-GPU loop ---------------------
+ * A part is an ordinary plan whose local numbering is
+ *   [replicated boundary nodes | halo, grouped by owner | owned rows]
+ * (paper_2107_03632_b200/multigpu.py:partition).  The reference has no
+ * multi-device path; these entry points add it.
+ *
+ * rbf_plan_set_halo: exchange lists of one part.  For peer i: send
+ * send_counts[i] owned values (local ids, concatenated in send_idx) and
+ * receive recv_counts[i] values into u[recv_offsets[i] ...] (its halo slice).
+ * rbf_group_create: nccl_uid != NULL -> one part per process, halos over NCCL
+ * (uid from rbf_nccl_unique_id on rank 0, broadcast by the caller); NULL ->
+ * all n_local parts live in this process and halos move by device copies.
+ * rbf_group_run: the loop of rbf_run over all parts: pack, exchange, step,
+ * all-reduce(max) of {residual bits, non-finite flag}, decide; bitwise equal
+ * to a single plan's run.  Fields are read / written per part with
+ * rbf_set_field / rbf_get_field (local numbering). */
+typedef struct rbf_group rbf_group;
+int rbf_nccl_unique_id(char* out128);
+int rbf_plan_set_halo(rbf_plan* plan, int32_t n_peers, const int32_t* peers,
+                      const int64_t* send_counts, const int64_t* send_idx,
+                      const int64_t* recv_counts, const int64_t* recv_offsets);
+int rbf_group_create(rbf_group** out, int32_t n_local, rbf_plan* const* plans,
+                     const int32_t* part_ids, const char* nccl_uid, int32_t rank,
+                     int32_t nranks);
+int rbf_group_run(rbf_group* group, double dt, int64_t steps, int32_t mode, double tol,
+                  int64_t max_steps, int64_t* steps_done, double* residual,
+                  int32_t* has_residual, int64_t* bad_step, double* device_seconds);
+void rbf_group_destroy(rbf_group* group);
+
 void rbf_plan_destroy(rbf_plan* plan);
 const char* rbf_last_error(void);
 int rbf_version(void);

@@ -42,6 +42,11 @@ EXPORTED = (
     "rbf_plan_destroy",
     "rbf_last_error",
     "rbf_version",
+    "rbf_nccl_unique_id",
+    "rbf_plan_set_halo",
+    "rbf_group_create",
+    "rbf_group_run",
+    "rbf_group_destroy",
 )
 
 
@@ -80,6 +85,15 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
             f"{p} not found: the CUDA library is not built "
             "(run `make -C paper_2107_03632_b200/csrc` or __graft_entry__.build())"
         )
+    if "RBFFD_NCCL_LIB" not in os.environ:  # the torch-bundled NCCL, loaded lazily by the library
+        try:
+            import nvidia.nccl as _nccl  # type: ignore
+
+            cand = Path(list(_nccl.__path__)[0]) / "lib" / "libnccl.so.2"
+            if cand.exists():
+                os.environ["RBFFD_NCCL_LIB"] = str(cand)
+        except Exception:
+            pass
     lib = ctypes.CDLL(str(p))
     vp, i64, i32, u32, dbl = (
         ctypes.c_void_p,
@@ -104,6 +118,11 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "rbf_plan_destroy": ([vp], None),
         "rbf_last_error": ([], ctypes.c_char_p),
         "rbf_version": ([], i32),
+        "rbf_nccl_unique_id": ([ctypes.c_char_p], i32),
+        "rbf_plan_set_halo": ([vp, i32, vp, vp, vp, vp, vp], i32),
+        "rbf_group_create": ([ctypes.POINTER(vp), i32, vp, vp, ctypes.c_char_p, i32, i32], i32),
+        "rbf_group_run": ([vp, dbl, i64, i32, dbl, i64, pi64, pdbl, pi32, pi64, pdbl], i32),
+        "rbf_group_destroy": ([vp], None),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

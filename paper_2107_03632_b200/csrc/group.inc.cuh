@@ -1,0 +1,322 @@
+// group.inc.cuh -- partitioned (multi-GPU) time loop; included by rbffd_b200.cu.
+//
+// nodes are partitioned across GPUs (paper_2107_03632_b200/
+// multigpu.py builds the parts); every part is an ordinary plan whose local
+// numbering is [replicated boundary | halo grouped by owner | owned rows].
+// Per step:  pack owned values the peers read -> exchange (NCCL send/recv,
+// or device copies when all parts live in this process) -> step kernel
+// (kDistributed epilogue: only red[] is accumulated) -> all-reduce(max) of
+// red[] = {residual bits, non-finite flag} -> decide_kernel applies the
+// reference's flag check / residual / steady break (solver.py:200-217)
+// identically on every part.  The j-order of every row is untouched: the
+// partitioned run is bitwise identical to a single-GPU run.
+//
+// NCCL is loaded at run time (dlopen) so the single-GPU library has no hard
+// dependency on it; the torch-bundled libnccl.so.2 (2.28.x) is used.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <map>
+
+namespace {
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi g_nccl;
+
+int load_nccl() {
+  if (g_nccl.h) return RBF_OK;
+  const char* env = std::getenv("RBFFD_NCCL_LIB");
+  void* h = env ? dlopen(env, RTLD_NOW | RTLD_GLOBAL) : nullptr;
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return fail(RBF_ERR_CUDA, std::string("cannot load NCCL: ") + dlerror());
+#define RBF_SYM(name, field)                                                         \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name));          \
+  if (!g_nccl.field) return fail(RBF_ERR_CUDA, std::string("NCCL symbol missing: ") + name);
+  RBF_SYM("ncclGetUniqueId", GetUniqueId)
+  RBF_SYM("ncclCommInitRank", CommInitRank)
+  RBF_SYM("ncclCommDestroy", CommDestroy)
+  RBF_SYM("ncclSend", Send)
+  RBF_SYM("ncclRecv", Recv)
+  RBF_SYM("ncclGroupStart", GroupStart)
+  RBF_SYM("ncclGroupEnd", GroupEnd)
+  RBF_SYM("ncclAllReduce", AllReduce)
+  RBF_SYM("ncclGetErrorString", GetErrorString)
+#undef RBF_SYM
+  g_nccl.h = h;
+  return RBF_OK;
+}
+
+#define RBF_NCK(call)                                                                      \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      return fail(RBF_ERR_CUDA, std::string(#call) + ": " + g_nccl.GetErrorString(r_));  \
+  } while (0)
+
+}  // namespace
+
+struct rbf_group {
+  std::vector<rbf_plan*> parts;   // parts living in this process
+  std::vector<int> ids;           // their global part ids
+  std::map<int, int> local_of;    // global id -> index in parts (local mode)
+  bool nccl = false;
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  int device = 0;
+  cudaStream_t stream = nullptr;  // every launch of the group runs here
+  rbf::DevStatus** d_status = nullptr;  // device array of the parts' status pointers
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+int group_pack(rbf_group* g, rbf_plan* p, int cur) {
+  if (p->halo_send_total == 0) return RBF_OK;
+  const int blocks = static_cast<int>(std::min<int64_t>((p->halo_send_total + 255) / 256, 148 * 8));
+  rbf::pack_halo_kernel<<<blocks, 256, 0, g->stream>>>(p->U[cur], p->halo_send_idx,
+                                                       p->halo_send_total, p->halo_sendbuf);
+  RBF_CK(cudaGetLastError());
+  ++p->launches;
+  return RBF_OK;
+}
+
+int group_exchange(rbf_group* g, int cur) {
+  if (g->nccl) {
+    rbf_plan* p = g->parts[0];
+    RBF_NCK(g_nccl.GroupStart());
+    for (size_t i = 0; i < p->halo_peers.size(); ++i) {
+      const int peer = p->halo_peers[i];
+      if (p->halo_send_count[i] > 0)
+        RBF_NCK(g_nccl.Send(p->halo_sendbuf + p->halo_send_off[i], p->halo_send_count[i],
+                            ncclFloat64, peer, g->comm, g->stream));
+      if (p->halo_recv_count[i] > 0)
+        RBF_NCK(g_nccl.Recv(p->U[cur] + p->halo_recv_off[i], p->halo_recv_count[i], ncclFloat64,
+                            peer, g->comm, g->stream));
+    }
+    RBF_NCK(g_nccl.GroupEnd());
+    return RBF_OK;
+  }
+  // in-process: copy each peer's packed segment straight into the halo slice
+  for (size_t a = 0; a < g->parts.size(); ++a) {
+    rbf_plan* p = g->parts[a];
+    for (size_t i = 0; i < p->halo_peers.size(); ++i) {
+      if (p->halo_recv_count[i] == 0) continue;
+      auto it = g->local_of.find(p->halo_peers[i]);
+      if (it == g->local_of.end()) return fail(RBF_ERR_PARAM, "peer part not in this group");
+      rbf_plan* q = g->parts[it->second];
+      int j = -1;
+      for (size_t k = 0; k < q->halo_peers.size(); ++k)
+        if (q->halo_peers[k] == g->ids[a]) j = static_cast<int>(k);
+      if (j < 0 || q->halo_send_count[j] != p->halo_recv_count[i])
+        return fail(RBF_ERR_PARAM, "halo lists of two parts disagree");
+      RBF_CK(cudaMemcpyPeerAsync(p->U[cur] + p->halo_recv_off[i], p->device,
+                                 q->halo_sendbuf + q->halo_send_off[j], q->device,
+                                 sizeof(double) * p->halo_recv_count[i], g->stream));
+    }
+  }
+  return RBF_OK;
+}
+
+int group_reduce_decide(rbf_group* g, int64_t step, int flags) {
+  if (g->nccl) {
+    rbf_plan* p = g->parts[0];
+    RBF_NCK(g_nccl.AllReduce(p->st->red, p->st->red, 2, ncclUint64, ncclMax, g->comm, g->stream));
+  } else if (g->parts.size() > 1) {
+    rbf::reduce_parts_kernel<<<1, 32, 0, g->stream>>>(g->d_status, static_cast<int>(g->parts.size()));
+    RBF_CK(cudaGetLastError());
+  }
+  for (rbf_plan* p : g->parts) {
+    rbf::decide_kernel<<<1, 32, 0, g->stream>>>(p->st, step, flags);
+    RBF_CK(cudaGetLastError());
+  }
+  return RBF_OK;
+}
+
+int group_step_kernel(rbf_group* g, rbf_plan* p, int cur, int flags) {
+  // the plan's own launch path, redirected to the group stream, without PDL
+  cudaStream_t saved = p->stream;
+  const bool pdl = p->pdl;
+  p->stream = g->stream;
+  p->pdl = false;
+  const int rc = launch_step(p, cur, flags);
+  p->stream = saved;
+  p->pdl = pdl;
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rbf_nccl_unique_id(char* out128) {
+  if (!out128) return fail(RBF_ERR_PARAM, "NULL argument");
+  RBF_TRY(load_nccl());
+  ncclUniqueId id;
+  RBF_NCK(g_nccl.GetUniqueId(&id));
+  std::memcpy(out128, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return RBF_OK;
+}
+
+int rbf_plan_set_halo(rbf_plan* p, int32_t n_peers, const int32_t* peers, const int64_t* send_counts,
+                      const int64_t* send_idx, const int64_t* recv_counts, const int64_t* recv_offsets) {
+  if (!p || n_peers < 0 || (n_peers > 0 && (!peers || !send_counts || !recv_counts || !recv_offsets)))
+    return fail(RBF_ERR_PARAM, "bad halo arguments");
+  RBF_CK(cudaSetDevice(p->device));
+  p->halo_peers.assign(peers, peers + n_peers);
+  p->halo_send_count.assign(send_counts, send_counts + n_peers);
+  p->halo_recv_count.assign(recv_counts, recv_counts + n_peers);
+  p->halo_recv_off.assign(recv_offsets, recv_offsets + n_peers);
+  p->halo_send_off.assign(n_peers, 0);
+  int64_t total = 0;
+  for (int i = 0; i < n_peers; ++i) {
+    if (send_counts[i] < 0 || recv_counts[i] < 0 || recv_offsets[i] < 0 ||
+        recv_offsets[i] + recv_counts[i] > p->B)
+      return fail(RBF_ERR_PARAM, "halo slice outside the non-owned range of the part");
+    p->halo_send_off[i] = total;
+    total += send_counts[i];
+  }
+  if (total > 0 && !send_idx) return fail(RBF_ERR_PARAM, "send_idx is NULL");
+  std::vector<int32_t> idx(static_cast<size_t>(total));
+  for (int64_t k = 0; k < total; ++k) {
+    if (send_idx[k] < p->B || send_idx[k] >= p->N)
+      return fail(RBF_ERR_PARAM, "a part can only send the values of rows it owns");
+    idx[k] = static_cast<int32_t>(send_idx[k]);
+  }
+  cudaFree(p->halo_send_idx);
+  cudaFree(p->halo_sendbuf);
+  p->halo_send_idx = nullptr;
+  p->halo_sendbuf = nullptr;
+  p->halo_send_total = total;
+  RBF_TRY(dev_alloc(p, &p->halo_send_idx, static_cast<size_t>(total)));
+  RBF_TRY(dev_alloc(p, &p->halo_sendbuf, static_cast<size_t>(total)));
+  if (total > 0)
+    RBF_CK(cudaMemcpy(p->halo_send_idx, idx.data(), sizeof(int32_t) * total, cudaMemcpyHostToDevice));
+  return RBF_OK;
+}
+
+int rbf_group_create(rbf_group** out, int32_t n_local, rbf_plan* const* plans, const int32_t* part_ids,
+                     const char* nccl_uid, int32_t rank, int32_t nranks) {
+  if (!out || n_local < 1 || !plans || !part_ids) return fail(RBF_ERR_PARAM, "bad group arguments");
+  *out = nullptr;
+  std::unique_ptr<rbf_group> g(new rbf_group());
+  g->nccl = nccl_uid != nullptr;
+  if (g->nccl && n_local != 1) return fail(RBF_ERR_PARAM, "an NCCL group holds one part per process");
+  for (int i = 0; i < n_local; ++i) {
+    if (!plans[i]) return fail(RBF_ERR_PARAM, "NULL plan");
+    if (plans[i]->device != plans[0]->device)
+      return fail(RBF_ERR_PARAM, "an in-process group keeps its parts on one device");
+    g->parts.push_back(plans[i]);
+    g->ids.push_back(part_ids[i]);
+    g->local_of[part_ids[i]] = i;
+  }
+  g->device = plans[0]->device;
+  g->rank = rank;
+  g->nranks = nranks;
+  RBF_CK(cudaSetDevice(g->device));
+  RBF_CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+  RBF_CK(cudaEventCreate(&g->ev0));
+  RBF_CK(cudaEventCreate(&g->ev1));
+  std::vector<rbf::DevStatus*> sts;
+  for (rbf_plan* p : g->parts) sts.push_back(p->st);
+  RBF_CK(cudaMalloc(&g->d_status, sizeof(rbf::DevStatus*) * sts.size()));
+  RBF_CK(cudaMemcpy(g->d_status, sts.data(), sizeof(rbf::DevStatus*) * sts.size(), cudaMemcpyHostToDevice));
+  if (g->nccl) {
+    RBF_TRY(load_nccl());
+    ncclUniqueId id;
+    std::memcpy(id.internal, nccl_uid, NCCL_UNIQUE_ID_BYTES);
+    RBF_NCK(g_nccl.CommInitRank(&g->comm, nranks, id, rank));
+  }
+  *out = g.release();
+  return RBF_OK;
+}
+
+int rbf_group_run(rbf_group* g, double dt, int64_t steps, int32_t mode, double tol, int64_t max_steps,
+                  int64_t* steps_done, double* residual, int32_t* has_residual, int64_t* bad_step,
+                  double* device_seconds) {
+  if (!g) return fail(RBF_ERR_PARAM, "group is NULL");
+  if (mode != RBF_MODE_FIXED && mode != RBF_MODE_STEADY) return fail(RBF_ERR_PARAM, "bad mode");
+  const bool steady = mode == RBF_MODE_STEADY;
+  const int64_t limit = steady ? max_steps : steps;
+  if (limit < 0) return fail(RBF_ERR_PARAM, "steps/max_steps must be >= 0");
+  RBF_CK(cudaSetDevice(g->device));
+  for (rbf_plan* p : g->parts) {
+    RBF_TRY(normalise_current(p));
+    RBF_TRY(reset_status(p, dt, tol));
+    RBF_CK(cudaStreamSynchronize(p->stream));
+  }
+  RBF_CK(cudaEventRecord(g->ev0, g->stream));
+  constexpr int64_t kPoll = 64;
+  for (int64_t s = 0; s < limit; ++s) {
+    const int cur = static_cast<int>(s & 1);
+    const bool need_res = steady || s == limit - 1;
+    const int flags = rbf::kDistributed | (need_res ? rbf::kNeedResidual : 0) | (steady ? rbf::kSteady : 0);
+    for (rbf_plan* p : g->parts) RBF_TRY(group_pack(g, p, cur));
+    RBF_TRY(group_exchange(g, cur));
+    for (rbf_plan* p : g->parts) RBF_TRY(group_step_kernel(g, p, cur, flags));
+    RBF_TRY(group_reduce_decide(g, s, flags));
+    if (steady && (s + 1) % kPoll == 0) {
+      rbf::DevStatus st;
+      RBF_CK(cudaMemcpyAsync(&st, g->parts[0]->st, sizeof(st), cudaMemcpyDeviceToHost, g->stream));
+      RBF_CK(cudaStreamSynchronize(g->stream));
+      if (st.bad_step >= 0 || st.conv_step >= 0) break;
+    }
+  }
+  RBF_CK(cudaEventRecord(g->ev1, g->stream));
+  RBF_CK(cudaStreamSynchronize(g->stream));
+  float ms = 0.f;
+  RBF_CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+  rbf_plan* p0 = g->parts[0];
+  RBF_TRY(read_status(p0));
+  const rbf::DevStatus s = *p0->h_st;
+  const int64_t done = limit > 0 ? s.step : 0;
+  bool have_res = false;
+  double res = 0.0;
+  if (s.last_res_step >= 0 && s.last_res_step == done - 1) {
+    double m;
+    std::memcpy(&m, &s.last_res_bits, sizeof(m));
+    res = m / dt;
+    have_res = true;
+  }
+  if (device_seconds) *device_seconds = ms * 1e-3;
+  if (bad_step) *bad_step = s.bad_step;
+  if (s.bad_step >= 0) {
+    for (rbf_plan* p : g->parts) p->cur = static_cast<int>((s.bad_step + 1) & 1);
+    if (steps_done) *steps_done = s.bad_step;
+    if (has_residual) *has_residual = 0;
+    return fail(RBF_ERR_INSTABILITY, "time loop unstable at step " + std::to_string(s.bad_step));
+  }
+  for (rbf_plan* p : g->parts) p->cur = static_cast<int>(done & 1);
+  if (steps_done) *steps_done = done;
+  if (residual) *residual = have_res ? res : 0.0;
+  if (has_residual) *has_residual = have_res ? 1 : 0;
+  if (steady && done == max_steps && (!have_res || !(res <= tol)))
+    return fail(RBF_ERR_TIMEOUT, "no steady state after " + std::to_string(done) + " steps");
+  return RBF_OK;
+}
+
+void rbf_group_destroy(rbf_group* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  if (g->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(g->comm);
+  cudaFree(g->d_status);
+  if (g->ev0) cudaEventDestroy(g->ev0);
+  if (g->ev1) cudaEventDestroy(g->ev1);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+}  // extern "C"

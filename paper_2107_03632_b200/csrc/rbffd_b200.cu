@@ -155,6 +155,12 @@ struct rbf_plan {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches = 0;
   int64_t device_bytes = 0;
+  // partitioned runs (group.inc.cuh): exchange lists of this part
+  std::vector<int> halo_peers;
+  std::vector<int64_t> halo_send_count, halo_send_off, halo_recv_count, halo_recv_off;
+  int* halo_send_idx = nullptr;     // [halo_send_total] local ids of owned nodes to send
+  double* halo_sendbuf = nullptr;   // packed values, segments per peer
+  int64_t halo_send_total = 0;
 
   rbf::StepArgs args() const {
     rbf::StepArgs a;
@@ -769,6 +775,8 @@ void rbf_plan_destroy(rbf_plan* p) {
   cudaFree(p->tmp);
   cudaFree(p->new_id);
   cudaFree(p->row_of_k);
+  cudaFree(p->halo_send_idx);
+  cudaFree(p->halo_sendbuf);
   cudaFree(p->st);
   if (p->h_st) cudaFreeHost(p->h_st);
   if (p->ev0) cudaEventDestroy(p->ev0);
@@ -778,3 +786,6 @@ void rbf_plan_destroy(rbf_plan* p) {
 }
 
 }  // extern "C"
+
+// ---- partitioned (multi-GPU) loop ------------------------------------------
+#include "group.inc.cuh"

@@ -39,6 +39,7 @@ struct DevStatus {
   unsigned int pad0;
   double dt;
   double tol;
+  unsigned long long red[2];         // distributed mode: [residual bits max, non-finite any]
 };
 
 struct StepArgs {
@@ -54,6 +55,8 @@ struct StepArgs {
 enum StepFlags : int {
   kNeedResidual = 1,  // compute max|u2-u1| for this step
   kSteady = 2,        // compare residual with tol and set conv_step
+  kDistributed = 4,   // partitioned run: only accumulate red[]; the group's
+                      // all-reduce + decide_kernel finalise the step
 };
 
 // ---- load helpers --------------------------------------------------------
@@ -123,10 +126,15 @@ __device__ __forceinline__ void step_epilogue(DevStatus* st, long long gstep, bo
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = (blockDim.x + 31) >> 5;
+  const bool dist = (flags & kDistributed) != 0;
   const int any_bad = __syncthreads_or(bad ? 1 : 0);
   if (any_bad && threadIdx.x == 0) {
-    atomicCAS(reinterpret_cast<unsigned long long*>(&st->bad_step),
-              static_cast<unsigned long long>(-1LL), static_cast<unsigned long long>(gstep));
+    if (dist) {
+      atomicMax(&st->red[1], 1ull);
+    } else {
+      atomicCAS(reinterpret_cast<unsigned long long*>(&st->bad_step),
+                static_cast<unsigned long long>(-1LL), static_cast<unsigned long long>(gstep));
+    }
   }
   if (flags & kNeedResidual) {
     unsigned long long m = warp_max_u64(dbits);
@@ -135,7 +143,7 @@ __device__ __forceinline__ void step_epilogue(DevStatus* st, long long gstep, bo
     if (warp == 0) {
       m = lane < nwarps ? s_max[lane] : 0ull;
       m = warp_max_u64(m);
-      if (lane == 0 && m != 0ull) atomicMax(&st->res_bits, m);
+      if (lane == 0 && m != 0ull) atomicMax(dist ? &st->red[0] : &st->res_bits, m);
     }
   }
   if (threadIdx.x == 0) {
@@ -146,7 +154,7 @@ __device__ __forceinline__ void step_epilogue(DevStatus* st, long long gstep, bo
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
     __threadfence();
-    if (flags & kNeedResidual) {
+    if ((flags & kNeedResidual) && !dist) {
       const unsigned long long m = atomicExch(&st->res_bits, 0ull);
       st->last_res_bits = m;
       st->last_res_step = gstep;
@@ -638,6 +646,48 @@ __global__ void scatter_field_kernel(const double* __restrict__ src, const int* 
     if (d1) d1[t] = src[i];
   }
 }
+// ---- partitioned (multi-GPU) loop helpers -----------------------------------
+// sendbuf[k] = u[idx[k]]: the owned values the peers read (their halo)
+__global__ void pack_halo_kernel(const double* __restrict__ u, const int* __restrict__ idx,
+                                 long long count, double* __restrict__ sendbuf) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < count;
+       k += static_cast<long long>(gridDim.x) * blockDim.x)
+    sendbuf[k] = u[idx[k]];
+}
+
+// In-process all-reduce(max) of red[] over the parts of a local group.
+__global__ void reduce_parts_kernel(DevStatus* const* st, int n_parts) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long m0 = 0, m1 = 0;
+  for (int p = 0; p < n_parts; ++p) {
+    m0 = st[p]->red[0] > m0 ? st[p]->red[0] : m0;
+    m1 = st[p]->red[1] > m1 ? st[p]->red[1] : m1;
+  }
+  for (int p = 0; p < n_parts; ++p) {
+    st[p]->red[0] = m0;
+    st[p]->red[1] = m1;
+  }
+}
+
+// After the all-reduce: the same decision on every part (solver.py:200-217).
+__global__ void decide_kernel(DevStatus* st, long long step, int flags) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const long long bs = st->bad_step, cs = st->conv_step;
+  if ((bs >= 0 && bs < step) || (cs >= 0 && cs < step)) return;  // already stopped
+  if (st->red[1]) {
+    st->bad_step = step;
+  } else if (flags & kNeedResidual) {
+    const unsigned long long m = st->red[0];
+    st->last_res_bits = m;
+    st->last_res_step = step;
+    if ((flags & kSteady) &&
+        __ddiv_rn(__longlong_as_double(static_cast<long long>(m)), st->dt) <= st->tol)
+      st->conv_step = step;
+  }
+  st->red[0] = 0;
+  st->red[1] = 0;
+}
+
 // F[row_of_k[k]] = f[k]
 __global__ void scatter_rows_kernel(const double* __restrict__ f, const long long* __restrict__ row_of_k,
                                     long long n_rows, double* __restrict__ F) {

@@ -1,0 +1,179 @@
+"""Node-partitioned multi-GPU path: host logic on CPU.
+
+* partition invariants (ownership, local numbering, symmetric exchange lists);
+* the partitioned loop emulated with the CPU oracle as each part's step --
+  in one process, and as a world-size-2 gloo job exchanging halos with
+  torch.distributed send/recv and all-reducing the residual -- must give the
+  single-process oracle's bits.  The device path of the same partition runs in
+  tests/test_parity_gpu.py (LocalGroup) on one GPU.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2107_03632_b200 as rb
+from paper_2107_03632_b200.multigpu import assemble_field, morton_codes, partition
+from oracle import oracle as orc
+
+
+def _problem(golden, name):
+    nodes, _, shapes, _ = golden(name)
+    interior = shapes.interior_nodes
+    rows = shapes.stencils.neighbors[interior]
+    f_int = rb.forcing(nodes.positions[interior])
+    return nodes, shapes, interior, rows, f_int
+
+
+@pytest.mark.parametrize("name,P", [("crit6", 2), ("crit6", 3), ("m6", 4), ("small", 5)])
+def test_partition_invariants(golden, name, P):
+    nodes, shapes, interior, rows, f_int = _problem(golden, name)
+    parts = partition(nodes.n_total, interior, rows, shapes.weights, f_int, nodes.positions, P)
+    owned = np.concatenate([p.rows_ref for p in parts])
+    assert np.array_equal(np.sort(owned), np.arange(interior.size))  # each row once
+    sizes = [p.n_own for p in parts]
+    assert max(sizes) - min(sizes) <= 1
+    for p in parts:
+        # local rows are the reference rows, renamed
+        assert np.array_equal(p.local_to_global[p.rows], rows[p.rows_ref])
+        assert np.array_equal(p.local_to_global[p.interior], interior[p.rows_ref])
+        assert np.array_equal(p.weights, shapes.weights[p.rows_ref])
+        assert np.array_equal(p.interior, np.arange(p.n_boundary + p.n_halo, p.n_local))
+        bnd = p.local_to_global[:p.n_boundary]
+        assert nodes.is_boundary[bnd].all() or not np.isin(bnd, interior).any()
+        for i, q in enumerate(p.peers):
+            other = parts[q]
+            j = other.peers.index(p.rank)
+            # what p receives from q is exactly what q sends to p, in order
+            assert p.recv_count[i] == other.send_idx[j].size
+            got = p.local_to_global[p.recv_offset[i]:p.recv_offset[i] + p.recv_count[i]]
+            sent = other.local_to_global[other.send_idx[j]]
+            assert np.array_equal(got, sent)
+            assert (other.send_idx[j] >= other.n_boundary + other.n_halo).all()
+
+
+def test_morton_codes_order_locality():
+    xy = np.array([[0.0, 0.0], [1.0, 1.0], [0.0, 1.0], [1.0, 0.0]])
+    c = morton_codes(xy)
+    assert c[0] < c[3] < c[2] < c[1]  # z-order: (0,0) (1,0) (0,1) (1,1)
+
+
+def _emulate(parts, u0, dt, steps):
+    """All parts in one process: oracle step per part, halos by copy."""
+    loc = [p.local_field(u0) for p in parts]
+    res = None
+    for s in range(steps):
+        for p, u in zip(parts, loc):  # exchange (reads the current field)
+            for i, q in enumerate(p.peers):
+                other = parts[q]
+                j = other.peers.index(p.rank)
+                u[p.recv_offset[i]:p.recv_offset[i] + p.recv_count[i]] = loc[q][other.send_idx[j]]
+        new = []
+        m = 0.0
+        for p, u in zip(parts, loc):
+            u2 = u.copy()
+            flags = orc.step_kernel(u, u2, p.interior, p.rows, p.weights, p.f_int, dt)
+            assert not flags.any()
+            own = slice(p.n_boundary + p.n_halo, None)
+            m = max(m, float(np.max(np.abs(u2[own] - u[own]))))
+            new.append(u2)
+        loc = new
+        res = m / dt
+    return assemble_field(parts, loc, u0), res
+
+
+@pytest.mark.parametrize("name,P,steps", [("crit6", 3, 100), ("m4", 4, 60), ("dome", 2, 300)])
+def test_partitioned_oracle_emulation_is_bitwise(golden, name, P, steps):
+    nodes, shapes, interior, rows, f_int = _problem(golden, name)
+    dt = 0.5 * rb.stability_bound(shapes)
+    u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    parts = partition(nodes.n_total, interior, rows, shapes.weights, f_int, nodes.positions, P)
+    field, res = _emulate(parts, u0, dt, steps)
+    want = orc.run_time_loop(nodes, shapes, dt=dt, steps=steps)
+    assert np.array_equal(field, want["field"])
+    assert res == want["residual"]
+
+
+def _gloo_worker(rank, world, port, name, steps, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from pathlib import Path
+
+        golden = Path(__file__).resolve().parent / "golden" / f"{name}.npz"
+        nodes, _, shapes = rb.load_fixture(golden)
+        interior = shapes.interior_nodes
+        rows = shapes.stencils.neighbors[interior]
+        f_int = rb.forcing(nodes.positions[interior])
+        dt = 0.5 * rb.stability_bound(shapes)
+        u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+        parts = partition(nodes.n_total, interior, rows, shapes.weights, f_int, nodes.positions, world)
+        p = parts[rank]
+        u = p.local_field(u0)
+        own = slice(p.n_boundary + p.n_halo, None)
+        res = None
+        for _ in range(steps):
+            ops = []
+            recv_bufs = []
+            for i, peer in enumerate(p.peers):
+                if p.send_idx[i].size:
+                    ops.append(dist.P2POp(dist.isend, torch.from_numpy(u[p.send_idx[i]].copy()), peer))
+                if p.recv_count[i]:
+                    buf = torch.empty(p.recv_count[i], dtype=torch.float64)
+                    recv_bufs.append((i, buf))
+                    ops.append(dist.P2POp(dist.irecv, buf, peer))
+            for r in dist.batch_isend_irecv(ops) if ops else []:
+                r.wait()
+            for i, buf in recv_bufs:
+                u[p.recv_offset[i]:p.recv_offset[i] + p.recv_count[i]] = buf.numpy()
+            u2 = u.copy()
+            bad = orc.step_kernel(u, u2, p.interior, p.rows, p.weights, p.f_int, dt).any()
+            red = torch.tensor([float(np.max(np.abs(u2[own] - u[own]))), float(bad)], dtype=torch.float64)
+            dist.all_reduce(red, op=dist.ReduceOp.MAX)  # exact: max
+            res = red[0].item() / dt
+            u = u2
+        owned = torch.from_numpy(np.ascontiguousarray(u[own]))
+        gathered = [torch.empty(pp.n_own, dtype=torch.float64) for pp in parts] if rank == 0 else None
+        if rank == 0:
+            gathered[0] = owned
+            for r in range(1, world):
+                dist.recv(gathered[r], r)
+            full = [np.concatenate([np.zeros(pp.n_boundary + pp.n_halo), g.numpy()]) for pp, g in zip(parts, gathered)]
+            field = assemble_field(parts, full, u0)
+            want = orc.run_time_loop(nodes, shapes, dt=dt, steps=steps)
+            q.put((bool(np.array_equal(field, want["field"])), res == want["residual"]))
+        else:
+            dist.send(owned, 0)
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.mark.parametrize("name,steps", [("crit6", 60)])
+def test_gloo_world2_partitioned_loop_is_bitwise(name, steps):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, name, steps, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=300)
+    assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
+    field_ok, res_ok = q.get(timeout=10)
+    assert field_ok and res_ok

@@ -341,3 +341,56 @@ def test_full_size_config2_matches_oracle(synth_cache):
     assert rep.residual == want["residual"]
     cb = rb.run_time_loop(cfg, nodes, shapes, copy_back=True)
     assert np.array_equal(cb.field, rep.field) and cb.residual == rep.residual
+
+
+# ---- node-partitioned loop on one device (multigpu.LocalGroup) ---------------
+@pytest.mark.parametrize("name,case,P", [
+    ("crit6", "fixed100", 1), ("crit6", "fixed100", 2), ("crit6", "fixed100", 3),
+    ("m6", "fixed100", 4), ("dome", "paper", 2), ("small", "steady", 2), ("dome", "steady", 3),
+])
+def test_partitioned_group_matches_reference(golden, manifest, name, case, P):
+    """The pack / exchange / step / all-reduce / decide sequence of the
+    multi-GPU path, all parts on one GPU: same bits as the reference."""
+    from paper_2107_03632_b200.multigpu import LocalGroup, partition, run_partitioned
+
+    nodes, _, shapes, z = golden(name)
+    meta = manifest[name][case]
+    interior = shapes.interior_nodes
+    rows = shapes.stencils.neighbors[interior]
+    parts = partition(nodes.n_total, interior, rows, shapes.weights,
+                      rb.forcing(nodes.positions[interior]), nodes.positions, P)
+    group = LocalGroup(parts)
+    cfg = config_for(nodes, shapes, meta)
+    field, steps, residual, _, dt = run_partitioned(group, nodes, shapes, cfg)
+    assert np.array_equal(field, z[f"{case}__field"])
+    assert steps == meta["steps"] and residual == meta["residual"] and dt == meta["dt"]
+    group.close()
+
+
+def test_partitioned_group_instability_and_synthetic(golden, synth_cache):
+    from paper_2107_03632_b200.multigpu import LocalGroup, partition, run_partitioned
+
+    nodes, _, shapes, _ = golden("crit6")
+    interior = shapes.interior_nodes
+    rows = shapes.stencils.neighbors[interior]
+    parts = partition(nodes.n_total, interior, rows, shapes.weights,
+                      rb.forcing(nodes.positions[interior]), nodes.positions, 3)
+    group = LocalGroup(parts)
+    want = orc.run_time_loop(nodes, shapes, dt=1.0, steps=500)
+    cfg = rb.SolveConfig(degree=2, support_size=15, nodes=2000, steps=500, dt=1.0)
+    with pytest.raises(rb.InstabilityError) as ei:
+        run_partitioned(group, nodes, shapes, cfg)
+    assert ei.value.step == want["step"]
+    group.close()
+
+    nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
+    interior = shapes.interior_nodes
+    rows = shapes.stencils.neighbors[interior]
+    parts = partition(nodes.n_total, interior, rows, shapes.weights,
+                      rb.forcing(nodes.positions[interior]), nodes.positions, 4)
+    group = LocalGroup(parts)
+    cfg = rb.SolveConfig(degree=2, support_size=15, nodes=200_000, steps=50)
+    field, steps, residual, _, _ = run_partitioned(group, nodes, shapes, cfg)
+    want = orc.run_time_loop(nodes, shapes, steps=50)
+    assert np.array_equal(field, want["field"]) and residual == want["residual"]
+    group.close()
