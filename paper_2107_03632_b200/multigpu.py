@@ -71,7 +71,7 @@ class Part:
     local_to_global: np.ndarray  # [n_local] global node id of each local node
     interior: np.ndarray  # [n_own] local ids (= B_p + H_p + r)
     rows: np.ndarray  # [n_own, n] local ids
-    weights: np.ndarray  # [n_own, n]
+    weights: Optional[np.ndarray]  # [n_own, n] (None: filled in later by the caller)
     f_int: np.ndarray  # [n_own]
     peers: List[int] = field(default_factory=list)  # sorted peer ranks
     send_idx: List[np.ndarray] = field(default_factory=list)  # per peer: local ids to send
@@ -95,6 +95,7 @@ def partition(n_total: int, interior: np.ndarray, rows: np.ndarray, weights: np.
     """Split the problem into `n_parts` row-balanced parts with halo lists.
 
     `rows` is the reference's ``neighbors[interior]`` (solver.py:182).
+    `weights` may be None when each rank assembles only its own rows' weights.
     """
     interior = np.ascontiguousarray(interior, dtype=np.int64)
     rows = np.ascontiguousarray(rows, dtype=np.int64)
@@ -144,7 +145,8 @@ def partition(n_total: int, interior: np.ndarray, rows: np.ndarray, weights: np.
         part = Part(
             rank=p, n_local=int(l2g.size), n_boundary=int(B), n_halo=int(H), rows_ref=ks,
             local_to_global=l2g, interior=np.arange(B + H, B + H + ks.size, dtype=np.int64),
-            rows=np.ascontiguousarray(local_rows), weights=np.ascontiguousarray(weights[ks]),
+            rows=np.ascontiguousarray(local_rows),
+            weights=None if weights is None else np.ascontiguousarray(weights[ks]),
             f_int=np.ascontiguousarray(np.asarray(f_int)[ks]),
         )
         groups = {}
