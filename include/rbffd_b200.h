@@ -80,6 +80,32 @@ int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n,
                     const double* weights, const double* f_int,
                     const double* positions, int32_t device, uint32_t flags);
 
+/*
+ * Weight assembly on the device: restates
+ * rbffd.weights._weights_batch (weights.py:218-259) -- PHS r^3 + monomials of
+ * `degree` (<= 6), support shifted to rows[k*n] and scaled by its radius, one
+ * saddle solve per row (Gaussian elimination with partial pivoting, one warp
+ * per system), weights rescaled by 1/radius^2.  Agrees with the reference's
+ * LAPACK solve to rounding (pinned by polynomial reproduction, like
+ * test_weights.py:51-104), not bit for bit.  A zero pivot or non-finite
+ * weight returns RBF_ERR_PARAM with *bad_row set (DegenerateStencilError,
+ * weights.py:183-192).
+ */
+int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows, int64_t N_i,
+                         int32_t n, int32_t degree, double* weights_out, int64_t* bad_row,
+                         int32_t device);
+
+/* rbf_plan_create with the weights assembled on the device straight into the
+ * SELL layout (the host never holds them; positions are required). */
+int rbf_plan_create_assembled(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, int32_t degree,
+                              const int64_t* interior, const int64_t* rows,
+                              const double* positions, const double* f_int, int32_t device,
+                              uint32_t flags);
+
+/* max_k sum_j |w_kj| of the plan's weights (stability_bound = 2 / this,
+ * solver.py:249-254), for plans whose weights never left the device. */
+int rbf_plan_weight_row_sum_max(rbf_plan* plan, double* out);
+
 /* Replace the per-row forcing (explicit_step's f[interior], solver.py:156). */
 int rbf_set_forcing(rbf_plan* plan, const double* f_int);
 

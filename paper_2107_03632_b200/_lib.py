@@ -47,6 +47,9 @@ EXPORTED = (
     "rbf_group_create",
     "rbf_group_run",
     "rbf_group_destroy",
+    "rbf_assemble_weights",
+    "rbf_plan_create_assembled",
+    "rbf_plan_weight_row_sum_max",
 )
 
 
@@ -123,6 +126,9 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "rbf_group_create": ([ctypes.POINTER(vp), i32, vp, vp, ctypes.c_char_p, i32, i32], i32),
         "rbf_group_run": ([vp, dbl, i64, i32, dbl, i64, pi64, pdbl, pi32, pi64, pdbl], i32),
         "rbf_group_destroy": ([vp], None),
+        "rbf_assemble_weights": ([vp, i64, vp, i64, i32, i32, vp, pi64, i32], i32),
+        "rbf_plan_create_assembled": ([ctypes.POINTER(vp), i64, i64, i32, i32, vp, vp, vp, vp, i32, u32], i32),
+        "rbf_plan_weight_row_sum_max": ([vp, pdbl], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

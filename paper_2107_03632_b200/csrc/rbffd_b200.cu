@@ -16,6 +16,7 @@
 //    step (last-CTA ticket), so the host only polls a 64-byte status per chunk.
 #include "../../include/rbffd_b200.h"
 #include "step_kernels.cuh"
+#include "weights_kernels.cuh"
 
 #include <cuda_runtime.h>
 
@@ -380,19 +381,70 @@ int rbf_version(void) { return 1; }
 
 const char* rbf_last_error(void) { return g_err.c_str(); }
 
-int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int64_t* interior,
-                    const int64_t* rows, const double* weights, const double* f_int,
-                    const double* positions, int32_t device, uint32_t flags) {
+}  // extern "C"
+
+namespace {
+
+// Monomial table of degree m (graded lex, x-exponent descending; weights.py:35-68).
+int fill_monomials(int degree, rbf::WeightArgs* wa) {
+  if (degree < 0 || degree > 6) return fail(RBF_ERR_PARAM, "degree must be in [0, 6]");
+  int k = 0;
+  for (int t = 0; t <= degree; ++t)
+    for (int ax = t; ax >= 0; --ax) {
+      wa->ex[k] = ax;
+      wa->ey[k] = t - ax;
+      wa->lap0[k] = ((ax == 2 && t == 2) || (ax == 0 && t == 2)) ? 2.0 : 0.0;
+      ++k;
+    }
+  wa->M = k;
+  return RBF_OK;
+}
+
+// Launch the weight assembly for `cnt` rows (device arrays); returns the
+// shared-memory size actually needed or an error.
+int launch_assemble(const double* d_pos, const long long* d_rows, long long cnt, long long k0, int n,
+                    const rbf::WeightArgs& proto, double* d_w, long long* d_bad, cudaStream_t stream) {
+  rbf::WeightArgs wa = proto;
+  wa.pos = d_pos;
+  wa.rows = d_rows;
+  wa.cnt = cnt;
+  wa.k0 = k0;
+  wa.n = n;
+  wa.w_out = d_w;
+  wa.bad_row = d_bad;
+  const int S = n + wa.M;
+  const size_t per_warp = (static_cast<size_t>(S) * (S + 1) + 2 * n) * sizeof(double);
+  int warps = static_cast<int>(std::min<size_t>(8, (200 * 1024) / per_warp));
+  if (warps < 1) return fail(RBF_ERR_PARAM, "support too large for on-chip weight assembly");
+  const size_t smem = per_warp * warps;
+  RBF_CK(cudaFuncSetAttribute(rbf::assemble_weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(smem)));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const long long blocks = std::min<long long>((cnt + warps - 1) / warps, static_cast<long long>(sms) * 8);
+  rbf::assemble_weights_kernel<<<static_cast<int>(std::max<long long>(blocks, 1)), 32 * warps, smem, stream>>>(wa);
+  RBF_CK(cudaGetLastError());
+  return RBF_OK;
+}
+
+int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int64_t* interior,
+                     const int64_t* rows, const double* weights, const double* f_int,
+                     const double* positions, int32_t device, uint32_t flags, int32_t degree) {
+  const bool assemble = degree >= 0;
   if (!out) return fail(RBF_ERR_PARAM, "out is NULL");
   *out = nullptr;
   if (N < 1 || N > std::numeric_limits<int32_t>::max())
     return fail(RBF_ERR_PARAM, "N must be in [1, 2^31-1]");
   if (N_i < 0 || N_i > N) return fail(RBF_ERR_PARAM, "need 0 <= N_i <= N");
   if (n < 1) return fail(RBF_ERR_PARAM, "support size n must be >= 1");
-  if (N_i > 0 && (!interior || !rows || !weights || !f_int))
+  if (N_i > 0 && (!interior || !rows || (!weights && !assemble) || !f_int))
     return fail(RBF_ERR_PARAM, "interior/rows/weights/f_int must be non-NULL");
   const bool morton = (flags & RBF_RENUMBER_MORTON) != 0;
-  if (morton && !positions) return fail(RBF_ERR_PARAM, "RBF_RENUMBER_MORTON needs positions");
+  if ((morton || assemble) && !positions)
+    return fail(RBF_ERR_PARAM, "RBF_RENUMBER_MORTON / weight assembly need positions");
+  rbf::WeightArgs wproto = {};
+  if (assemble) RBF_TRY(fill_monomials(degree, &wproto));
+  if (assemble && n < wproto.M) return fail(RBF_ERR_PARAM, "support size below the monomial count");
 
   // ---- host-side validation + renumbering ----------------------------------
   const int64_t B = N - N_i;
@@ -485,6 +537,15 @@ int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int
   int* d_err = nullptr;
   RBF_CK(cudaMalloc(&d_err, sizeof(int)));
   RBF_CK(cudaMemset(d_err, 0, sizeof(int)));
+  double* d_pos = nullptr;
+  long long* d_bad = nullptr;
+  if (assemble && N_i > 0) {
+    RBF_CK(cudaMalloc(&d_pos, sizeof(double) * 2 * N));
+    RBF_CK(cudaMemcpy(d_pos, positions, sizeof(double) * 2 * N, cudaMemcpyHostToDevice));
+    RBF_CK(cudaMalloc(&d_bad, sizeof(long long)));
+    const long long none = std::numeric_limits<long long>::max();
+    RBF_CK(cudaMemcpy(d_bad, &none, sizeof(none), cudaMemcpyHostToDevice));
+  }
   if (N_i > 0) {
     const int64_t chunk_rows = std::max<int64_t>(1, (int64_t(1) << 25) / n);
     const int64_t cap = std::min<int64_t>(chunk_rows, N_i);
@@ -496,8 +557,12 @@ int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int
     RBF_CK(cudaMalloc(&d_f, sizeof(double) * cap));
     for (int64_t k0 = 0; k0 < N_i; k0 += cap) {
       const int64_t cnt = std::min<int64_t>(cap, N_i - k0);
-      RBF_CK(cudaMemcpyAsync(d_w, weights + k0 * n, sizeof(double) * cnt * n, cudaMemcpyHostToDevice, p->stream));
       RBF_CK(cudaMemcpyAsync(d_c, rows + k0 * n, sizeof(long long) * cnt * n, cudaMemcpyHostToDevice, p->stream));
+      if (assemble) {  // weights computed on the device, never on the host
+        RBF_TRY(launch_assemble(d_pos, d_c, cnt, k0, n, wproto, d_w, d_bad, p->stream));
+      } else {
+        RBF_CK(cudaMemcpyAsync(d_w, weights + k0 * n, sizeof(double) * cnt * n, cudaMemcpyHostToDevice, p->stream));
+      }
       RBF_CK(cudaMemcpyAsync(d_f, f_int + k0, sizeof(double) * cnt, cudaMemcpyHostToDevice, p->stream));
       const int64_t total = cnt * n;
       const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 32));
@@ -513,6 +578,16 @@ int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int
   int h_err = 0;
   RBF_CK(cudaMemcpy(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
   cudaFree(d_err);
+  if (d_bad) {
+    long long bad = 0;
+    RBF_CK(cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost));
+    cudaFree(d_bad);
+    cudaFree(d_pos);
+    if (bad != std::numeric_limits<long long>::max()) {
+      rbf_plan_destroy(p.release());
+      return fail(RBF_ERR_PARAM, "degenerate stencil at interior row " + std::to_string(bad));
+    }
+  }
   if (h_err) {
     rbf_plan_destroy(p.release());
     return fail(RBF_ERR_PARAM, "stencil node id out of range");
@@ -575,6 +650,96 @@ int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int
   }
   RBF_CK(cudaStreamSynchronize(p->stream));
   *out = p.release();
+  return RBF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int64_t* interior,
+                    const int64_t* rows, const double* weights, const double* f_int,
+                    const double* positions, int32_t device, uint32_t flags) {
+  return plan_create_impl(out, N, N_i, n, interior, rows, weights, f_int, positions, device, flags, -1);
+}
+
+int rbf_plan_create_assembled(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, int32_t degree,
+                              const int64_t* interior, const int64_t* rows, const double* positions,
+                              const double* f_int, int32_t device, uint32_t flags) {
+  if (degree < 0) return fail(RBF_ERR_PARAM, "degree must be >= 0");
+  return plan_create_impl(out, N, N_i, n, interior, rows, nullptr, f_int, positions, device, flags,
+                          degree);
+}
+
+int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows, int64_t N_i,
+                         int32_t n, int32_t degree, double* weights_out, int64_t* bad_row,
+                         int32_t device) {
+  if (!positions || (N_i > 0 && (!rows || !weights_out)) || n < 1 || N < 1)
+    return fail(RBF_ERR_PARAM, "bad arguments");
+  rbf::WeightArgs wproto = {};
+  RBF_TRY(fill_monomials(degree, &wproto));
+  if (n < wproto.M) return fail(RBF_ERR_PARAM, "support size below the monomial count");
+  if (bad_row) *bad_row = -1;
+  if (N_i == 0) return RBF_OK;
+  for (int64_t e = 0; e < N_i * n; ++e)
+    if (rows[e] < 0 || rows[e] >= N) return fail(RBF_ERR_PARAM, "stencil node id out of range");
+  RBF_CK(cudaSetDevice(device));
+  cudaStream_t st;
+  RBF_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  double* d_pos = nullptr;
+  long long* d_rows = nullptr;
+  double* d_w = nullptr;
+  long long* d_bad = nullptr;
+  const int64_t cap = std::min<int64_t>(N_i, std::max<int64_t>(1, (int64_t(1) << 24) / n));
+  RBF_CK(cudaMalloc(&d_pos, sizeof(double) * 2 * N));
+  RBF_CK(cudaMalloc(&d_rows, sizeof(long long) * cap * n));
+  RBF_CK(cudaMalloc(&d_w, sizeof(double) * cap * n));
+  RBF_CK(cudaMalloc(&d_bad, sizeof(long long)));
+  const long long none = std::numeric_limits<long long>::max();
+  RBF_CK(cudaMemcpy(d_bad, &none, sizeof(none), cudaMemcpyHostToDevice));
+  RBF_CK(cudaMemcpy(d_pos, positions, sizeof(double) * 2 * N, cudaMemcpyHostToDevice));
+  int rc = RBF_OK;
+  for (int64_t k0 = 0; k0 < N_i && rc == RBF_OK; k0 += cap) {
+    const int64_t cnt = std::min<int64_t>(cap, N_i - k0);
+    if (cudaMemcpyAsync(d_rows, rows + k0 * n, sizeof(long long) * cnt * n, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+      rc = fail(RBF_ERR_CUDA, "upload rows");
+      break;
+    }
+    rc = launch_assemble(d_pos, d_rows, cnt, k0, n, wproto, d_w, d_bad, st);
+    if (rc == RBF_OK && cudaMemcpyAsync(weights_out + k0 * n, d_w, sizeof(double) * cnt * n,
+                                        cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      rc = fail(RBF_ERR_CUDA, "download weights");
+  }
+  if (rc == RBF_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBF_ERR_CUDA, "assembly");
+  long long bad = none;
+  if (rc == RBF_OK) cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost);
+  cudaFree(d_pos);
+  cudaFree(d_rows);
+  cudaFree(d_w);
+  cudaFree(d_bad);
+  cudaStreamDestroy(st);
+  if (rc != RBF_OK) return rc;
+  if (bad != none) {
+    if (bad_row) *bad_row = bad;
+    return fail(RBF_ERR_PARAM, "degenerate stencil at interior row " + std::to_string(bad));
+  }
+  return RBF_OK;
+}
+
+int rbf_plan_weight_row_sum_max(rbf_plan* p, double* out) {
+  if (!p || !out) return fail(RBF_ERR_PARAM, "NULL argument");
+  RBF_CK(cudaSetDevice(p->device));
+  double* d = nullptr;
+  RBF_CK(cudaMalloc(&d, sizeof(double)));
+  RBF_CK(cudaMemsetAsync(d, 0, sizeof(double), p->stream));
+  const int blocks = static_cast<int>(std::min<int64_t>((p->N_i + 255) / 256, 148 * 8));
+  if (p->N_i > 0) {
+    rbf::row_abs_sum_max_kernel<<<blocks, 256, 0, p->stream>>>(p->W, p->N_i, p->n, d);
+    RBF_CK(cudaGetLastError());
+  }
+  RBF_CK(cudaMemcpyAsync(out, d, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  cudaFree(d);
   return RBF_OK;
 }
 

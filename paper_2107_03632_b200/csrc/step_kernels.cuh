@@ -688,6 +688,23 @@ __global__ void decide_kernel(DevStatus* st, long long step, int flags) {
   st->red[1] = 0;
 }
 
+// max_r sum_j |w_rj| over the SELL rows (stability_bound, solver.py:249-254;
+// serial j sum per row, then an exact max over non-negative bit patterns)
+__global__ void row_abs_sum_max_kernel(const double* __restrict__ W, long long n_rows, int n,
+                                       double* out) {
+  unsigned long long m = 0ull;
+  for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < n_rows;
+       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long base = (r >> 5) * static_cast<long long>(n) * 32 + (r & 31);
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s += fabs(W[base + 32LL * j]);
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(s));
+    m = b > m ? b : m;
+  }
+  m = warp_max_u64(m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(reinterpret_cast<unsigned long long*>(out), m);
+}
+
 // F[row_of_k[k]] = f[k]
 __global__ void scatter_rows_kernel(const double* __restrict__ f, const long long* __restrict__ row_of_k,
                                     long long n_rows, double* __restrict__ F) {

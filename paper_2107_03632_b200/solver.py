@@ -190,6 +190,38 @@ class Plan:
         self.n = int(n)
         self._finalizer = weakref.finalize(self, self._lib.rbf_plan_destroy, handle)
 
+    @classmethod
+    def assembled(cls, n_total, interior, rows, positions, f_int, degree: int, *,
+                  renumber: bool = False, device: int = 0, resident: bool = True,
+                  pdl: bool = True, tma: bool = True) -> "Plan":
+        """Plan whose weights are assembled on the device (rbf_plan_create_assembled):
+        the PHS+monomial solves of weights.py:218-259 run on the GPU straight into
+        the SELL layout; the host never holds the weights."""
+        self = cls.__new__(cls)
+        self._lib = _lib.load()
+        interior = _as(interior, np.int64)
+        rows = _as(rows, np.int64)
+        f_int = _as(f_int, np.float64)
+        pos = _as(positions, np.float64)
+        n_rows, n = rows.shape
+        flags = (_lib.RBF_RENUMBER_MORTON if renumber else 0) | (0 if resident else _lib.RBF_NO_RESIDENT) \
+            | (0 if pdl else _lib.RBF_NO_PDL) | (0 if tma else _lib.RBF_STREAM_LDG)
+        handle = ctypes.c_void_p()
+        rc = self._lib.rbf_plan_create_assembled(
+            ctypes.byref(handle), int(n_total), int(n_rows), int(n), int(degree), _ptr(interior),
+            _ptr(rows), _ptr(pos), _ptr(f_int), int(device), flags)
+        self._check(rc)
+        self._h = handle
+        self.n_total, self.n_rows, self.n = int(n_total), int(n_rows), int(n)
+        self._finalizer = weakref.finalize(self, self._lib.rbf_plan_destroy, handle)
+        return self
+
+    def weight_row_sum_max(self) -> float:
+        """max_k sum_j |w_kj| on the device (stability_bound = 2 / this)."""
+        out = ctypes.c_double()
+        self._check(self._lib.rbf_plan_weight_row_sum_max(self._h, ctypes.byref(out)))
+        return out.value
+
     # -- plumbing ------------------------------------------------------------
     def _check(self, rc: int) -> int:
         if rc == _lib.RBF_OK or rc in (_lib.RBF_ERR_INSTABILITY, _lib.RBF_ERR_TIMEOUT):

@@ -141,9 +141,17 @@ def laplacian_weights(nodes: NodeSet, stencils: StencilSet, degree: int,
     return ShapeStore(degree=degree, interior_nodes=interior, weights=weights, stencils=stencils)
 
 
-def synthetic_problem(target: int, n: int, degree: int, seed: int = 1):
-    """(nodes, stencils, shapes) of a synthetic scattered-node disk."""
+def synthetic_problem(target: int, n: int, degree: int, seed: int = 1, weights: str = "cpu"):
+    """(nodes, stencils, shapes) of a synthetic scattered-node disk.
+
+    weights="cpu": numpy/LAPACK restatement above; "gpu": the device assembly
+    (paper_2107_03632_b200.weights, minutes -> seconds at 1e7 rows)."""
     nodes = disk_nodes(target, seed)
     stencils = knn_stencils(nodes, n)
-    shapes = laplacian_weights(nodes, stencils, degree)
+    if weights == "gpu":
+        from .weights import assemble_shapes
+
+        shapes = assemble_shapes(nodes, stencils, degree)
+    else:
+        shapes = laplacian_weights(nodes, stencils, degree)
     return nodes, stencils, shapes
