@@ -57,7 +57,8 @@ def build_problem(workload: str, seed: int = 1):
     target, n, m, _ = WORKLOADS[workload]
     if workload == "c1":
         return rb.load_fixture(ROOT / "tests" / "golden" / "dome.npz")
-    return synth.synthetic_problem(target, n, m, seed=seed)
+    # nodes + kNN on the CPU (scipy), weights assembled on the GPU
+    return synth.synthetic_problem(target, n, m, seed=seed, weights="gpu")
 
 
 def measured_peak():

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -108,6 +109,19 @@ bool pick_kernels(int n, int rpl_req, StreamFn* s, ResidentFn* r, TmaFn* t, int*
       return false;
   }
 }
+
+// RBFFD_VERBOSE=1: phase timings of plan construction on stderr
+struct PhaseTimer {
+  bool on = std::getenv("RBFFD_VERBOSE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[rbffd] %-28s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
 
 uint64_t morton2(uint32_t x, uint32_t y) {
   auto spread = [](uint64_t v) {
@@ -447,6 +461,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   if (assemble && n < wproto.M) return fail(RBF_ERR_PARAM, "support size below the monomial count");
 
   // ---- host-side validation + renumbering ----------------------------------
+  PhaseTimer timer;
   const int64_t B = N - N_i;
   std::vector<uint8_t> seen(static_cast<size_t>(N), 0);
   bool identity = !morton;
@@ -494,6 +509,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   }
   seen.clear();
   seen.shrink_to_fit();
+  timer.mark("validate + renumber (host)");
 
   std::unique_ptr<rbf_plan> p(new rbf_plan());
   p->device = device;
@@ -522,6 +538,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   RBF_CK(cudaMemsetAsync(p->U[0], 0, static_cast<size_t>(N) * sizeof(double), p->stream));
   RBF_CK(cudaMemsetAsync(p->U[1], 0, static_cast<size_t>(N) * sizeof(double), p->stream));
 
+  timer.mark("alloc + memset");
   // ---- device-side SELL-32 packing, in row chunks ---------------------------
   long long* d_row_of_k = nullptr;
   if (!identity) {
@@ -575,6 +592,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
     cudaFree(d_c);
     cudaFree(d_f);
   }
+  timer.mark("upload + pack");
   int h_err = 0;
   RBF_CK(cudaMemcpy(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
   cudaFree(d_err);
@@ -649,6 +667,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
     p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));
   }
   RBF_CK(cudaStreamSynchronize(p->stream));
+  timer.mark("kernel selection");
   *out = p.release();
   return RBF_OK;
 }

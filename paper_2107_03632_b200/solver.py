@@ -312,7 +312,7 @@ def _plan_for(shapes, n_total: int, f_int: np.ndarray, positions=None, *, cache:
             plan = hit[1]
             plan.set_forcing(f_int)
             return plan
-    rows = np.ascontiguousarray(neighbors[interior])  # solver.py:182
+    rows = _interior_rows(neighbors, interior)  # solver.py:182
     plan = Plan(n_total, interior, rows, weights, f_int, positions, renumber=renumber)
     if cache:
         try:
@@ -321,6 +321,17 @@ def _plan_for(shapes, n_total: int, f_int: np.ndarray, positions=None, *, cache:
             return plan
         _PLANS[key] = (ref, plan)
     return plan
+
+
+def _interior_rows(neighbors: np.ndarray, interior: np.ndarray) -> np.ndarray:
+    """neighbors[interior] (solver.py:182) -- a view, not a copy, when the
+    interior is the contiguous tail [B, N) as in generated node sets."""
+    n_i = interior.size
+    B = neighbors.shape[0] - n_i
+    if n_i and interior[0] == B and interior[-1] == neighbors.shape[0] - 1 and \
+            np.array_equal(interior, np.arange(B, B + n_i)):
+        return np.ascontiguousarray(neighbors[B:])
+    return np.ascontiguousarray(neighbors[interior])
 
 
 def clear_plan_cache() -> None:
