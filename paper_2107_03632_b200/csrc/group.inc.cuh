@@ -195,15 +195,15 @@ int rbf_plan_set_halo(rbf_plan* p, int32_t n_peers, const int32_t* peers, const 
       return fail(RBF_ERR_PARAM, "a part can only send the values of rows it owns");
     idx[k] = static_cast<int32_t>(send_idx[k]);
   }
-  cudaFree(p->halo_send_idx);
-  cudaFree(p->halo_sendbuf);
-  p->halo_send_idx = nullptr;
-  p->halo_sendbuf = nullptr;
+  pool_free(p->halo_send_idx, p->stream);
+  pool_free(p->halo_sendbuf, p->stream);
   p->halo_send_total = total;
   RBF_TRY(dev_alloc(p, &p->halo_send_idx, static_cast<size_t>(total)));
   RBF_TRY(dev_alloc(p, &p->halo_sendbuf, static_cast<size_t>(total)));
   if (total > 0)
-    RBF_CK(cudaMemcpy(p->halo_send_idx, idx.data(), sizeof(int32_t) * total, cudaMemcpyHostToDevice));
+    RBF_CK(cudaMemcpyAsync(p->halo_send_idx, idx.data(), sizeof(int32_t) * total, cudaMemcpyHostToDevice,
+                           p->stream));
+  RBF_CK(cudaStreamSynchronize(p->stream));
   return RBF_OK;
 }
 

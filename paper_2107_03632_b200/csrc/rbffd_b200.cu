@@ -24,10 +24,12 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <parallel/algorithm>
 #include <string>
 #include <vector>
@@ -46,6 +48,12 @@ int fail(int code, const std::string& msg) {
     cudaError_t e_ = (call);                                                                 \
     if (e_ != cudaSuccess)                                                                   \
       return fail(RBF_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+#define RBF_TRY(expr)          \
+  do {                         \
+    int rc_ = (expr);          \
+    if (rc_ != RBF_OK) return rc_; \
   } while (0)
 
 constexpr int kGraphSteps = 64;  // steps per captured graph (even: keeps buffer parity)
@@ -192,19 +200,76 @@ struct rbf_plan {
 
 namespace {
 
-template <typename T>
-int dev_alloc(rbf_plan* p, T** ptr, size_t count) {
-  if (count == 0) count = 1;
-  RBF_CK(cudaMalloc(reinterpret_cast<void**>(ptr), count * sizeof(T)));
-  p->device_bytes += static_cast<int64_t>(count * sizeof(T));
+// Device memory comes from the stream-ordered default pool of the device,
+// with the release threshold raised so freed plan memory stays mapped and the
+// next plan reuses it (cudaMalloc/cudaFree of hundreds of MB cost 10-1000 ms
+// per plan on B200; profiles/README.md).
+int prepare_pool(int device) {
+  static bool done[64] = {false};
+  if (device >= 0 && device < 64 && !done[device]) {
+    cudaMemPool_t pool;
+    RBF_CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    RBF_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    done[device] = true;
+  }
   return RBF_OK;
 }
 
-#define RBF_TRY(expr)          \
-  do {                         \
-    int rc_ = (expr);          \
-    if (rc_ != RBF_OK) return rc_; \
-  } while (0)
+template <typename T>
+int pool_alloc(T** ptr, size_t count, cudaStream_t s) {
+  if (count == 0) count = 1;
+  RBF_CK(cudaMallocAsync(reinterpret_cast<void**>(ptr), count * sizeof(T), s));
+  return RBF_OK;
+}
+
+template <typename T>
+void pool_free(T*& ptr, cudaStream_t s) {
+  if (ptr) cudaFreeAsync(ptr, s);
+  ptr = nullptr;
+}
+
+template <typename T>
+int dev_alloc(rbf_plan* p, T** ptr, size_t count) {
+  RBF_TRY(pool_alloc(ptr, count, p->stream));
+  p->device_bytes += static_cast<int64_t>((count ? count : 1) * sizeof(T));
+  return RBF_OK;
+}
+
+// Pinned, double-buffered staging for plan uploads: the host copies (and
+// int64 -> int32 id conversion) of chunk c+1 run while chunk c is on the bus.
+struct Staging {
+  std::mutex mu;
+  unsigned char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  size_t cap = 0;
+  int device = -1;
+};
+
+Staging& staging() {
+  static Staging s;
+  return s;
+}
+
+int staging_acquire(Staging& sg, int device) {
+  constexpr size_t kCap = size_t(64) << 20;
+  if (sg.cap == kCap && sg.device == device) return RBF_OK;
+  for (int b = 0; b < 2; ++b) {
+    if (sg.buf[b]) cudaFreeHost(sg.buf[b]);
+    if (sg.ev[b]) cudaEventDestroy(sg.ev[b]);
+    sg.buf[b] = nullptr;
+    sg.ev[b] = nullptr;
+  }
+  sg.cap = 0;
+  for (int b = 0; b < 2; ++b) {
+    RBF_CK(cudaMallocHost(reinterpret_cast<void**>(&sg.buf[b]), kCap));
+    RBF_CK(cudaEventCreateWithFlags(&sg.ev[b], cudaEventDisableTiming));
+  }
+  sg.cap = kCap;
+  sg.device = device;
+  return RBF_OK;
+}
+
 
 // One streaming step: reads U[in], writes U[1-in].
 int launch_step(rbf_plan* p, int in, int flags) {
@@ -302,7 +367,9 @@ int normalise_current(rbf_plan* p) {
 int run_streaming(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
   const int step_flags = steady ? (rbf::kNeedResidual | rbf::kSteady) : 0;
   cudaGraphExec_t graph = nullptr;
+  PhaseTimer timer;
   if (limit > kGraphSteps) RBF_TRY(get_graph(p, copy_back, steady, &graph));
+  timer.mark("graph capture/instantiate");
   RBF_CK(cudaEventRecord(p->ev0, p->stream));
   int64_t launched = 0;
   if (!steady) {
@@ -318,6 +385,7 @@ int run_streaming(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
       else RBF_TRY(launch_step(p, static_cast<int>(launched & 1), fl));
     }
     RBF_CK(cudaEventRecord(p->ev1, p->stream));
+    timer.mark("enqueue");
     return RBF_OK;
   }
   // Steady: poll the device status once per chunk, keeping two chunks in
@@ -416,7 +484,7 @@ int fill_monomials(int degree, rbf::WeightArgs* wa) {
 
 // Launch the weight assembly for `cnt` rows (device arrays); returns the
 // shared-memory size actually needed or an error.
-int launch_assemble(const double* d_pos, const long long* d_rows, long long cnt, long long k0, int n,
+int launch_assemble(const double* d_pos, const int* d_rows, long long cnt, long long k0, int n,
                     const rbf::WeightArgs& proto, double* d_w, long long* d_bad, cudaStream_t stream) {
   rbf::WeightArgs wa = proto;
   wa.pos = d_pos;
@@ -521,6 +589,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   p->renumbered = !identity;
   p->pdl = (flags & RBF_NO_PDL) == 0;
   RBF_CK(cudaSetDevice(device));
+  RBF_TRY(prepare_pool(device));
   RBF_CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   RBF_CK(cudaEventCreate(&p->ev0));
   RBF_CK(cudaEventCreate(&p->ev1));
@@ -532,75 +601,113 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   RBF_TRY(dev_alloc(p.get(), &p->F, static_cast<size_t>(p->S) * 32));
   RBF_TRY(dev_alloc(p.get(), &p->U[0], static_cast<size_t>(N)));
   RBF_TRY(dev_alloc(p.get(), &p->U[1], static_cast<size_t>(N)));
-  RBF_CK(cudaMemsetAsync(p->W, 0, sell * sizeof(double), p->stream));
-  RBF_CK(cudaMemsetAsync(p->C, 0, sell * sizeof(int), p->stream));
-  RBF_CK(cudaMemsetAsync(p->F, 0, static_cast<size_t>(p->S) * 32 * sizeof(double), p->stream));
+  // padding lanes of the last slice are never consumed (every kernel masks
+  // r >= N_i), so only the field buffers are cleared
   RBF_CK(cudaMemsetAsync(p->U[0], 0, static_cast<size_t>(N) * sizeof(double), p->stream));
   RBF_CK(cudaMemsetAsync(p->U[1], 0, static_cast<size_t>(N) * sizeof(double), p->stream));
+  timer.mark("alloc");
 
-  timer.mark("alloc + memset");
-  // ---- device-side SELL-32 packing, in row chunks ---------------------------
+  // ---- device-side SELL-32 packing, in row chunks through pinned staging ----
   long long* d_row_of_k = nullptr;
   if (!identity) {
     RBF_TRY(dev_alloc(p.get(), &p->new_id, static_cast<size_t>(N)));
     RBF_TRY(dev_alloc(p.get(), &p->tmp, static_cast<size_t>(N)));
-    RBF_CK(cudaMemcpy(p->new_id, new_id.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+    RBF_CK(cudaMemcpyAsync(p->new_id, new_id.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, p->stream));
     if (N_i > 0) {
       RBF_TRY(dev_alloc(p.get(), &p->row_of_k, static_cast<size_t>(N_i)));
       d_row_of_k = p->row_of_k;
-      RBF_CK(cudaMemcpy(d_row_of_k, row_of_k.data(), sizeof(long long) * N_i, cudaMemcpyHostToDevice));
+      RBF_CK(cudaMemcpyAsync(d_row_of_k, row_of_k.data(), sizeof(long long) * N_i, cudaMemcpyHostToDevice,
+                             p->stream));
     }
   }
   int* d_err = nullptr;
-  RBF_CK(cudaMalloc(&d_err, sizeof(int)));
-  RBF_CK(cudaMemset(d_err, 0, sizeof(int)));
+  RBF_TRY(pool_alloc(&d_err, 1, p->stream));
+  RBF_CK(cudaMemsetAsync(d_err, 0, sizeof(int), p->stream));
   double* d_pos = nullptr;
   long long* d_bad = nullptr;
   if (assemble && N_i > 0) {
-    RBF_CK(cudaMalloc(&d_pos, sizeof(double) * 2 * N));
-    RBF_CK(cudaMemcpy(d_pos, positions, sizeof(double) * 2 * N, cudaMemcpyHostToDevice));
-    RBF_CK(cudaMalloc(&d_bad, sizeof(long long)));
+    RBF_TRY(pool_alloc(&d_pos, static_cast<size_t>(2 * N), p->stream));
+    RBF_CK(cudaMemcpyAsync(d_pos, positions, sizeof(double) * 2 * N, cudaMemcpyHostToDevice, p->stream));
+    RBF_TRY(pool_alloc(&d_bad, 1, p->stream));
     const long long none = std::numeric_limits<long long>::max();
-    RBF_CK(cudaMemcpy(d_bad, &none, sizeof(none), cudaMemcpyHostToDevice));
+    RBF_CK(cudaMemcpyAsync(d_bad, &none, sizeof(none), cudaMemcpyHostToDevice, p->stream));
+    RBF_CK(cudaStreamSynchronize(p->stream));  // `none` lives on this stack frame
   }
+  bool ids_ok = true;
   if (N_i > 0) {
-    const int64_t chunk_rows = std::max<int64_t>(1, (int64_t(1) << 25) / n);
-    const int64_t cap = std::min<int64_t>(chunk_rows, N_i);
+    Staging& sg = staging();
+    std::lock_guard<std::mutex> lock(sg.mu);
+    RBF_TRY(staging_acquire(sg, device));
+    const size_t row_bytes = static_cast<size_t>(n) * (assemble ? 4 : 12) + 8;
+    const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(N_i, static_cast<int64_t>(sg.cap / row_bytes)));
     double* d_w = nullptr;
-    long long* d_c = nullptr;
+    int* d_c = nullptr;
     double* d_f = nullptr;
-    RBF_CK(cudaMalloc(&d_w, sizeof(double) * cap * n));
-    RBF_CK(cudaMalloc(&d_c, sizeof(long long) * cap * n));
-    RBF_CK(cudaMalloc(&d_f, sizeof(double) * cap));
-    for (int64_t k0 = 0; k0 < N_i; k0 += cap) {
+    RBF_TRY(pool_alloc(&d_w, static_cast<size_t>(cap) * n, p->stream));
+    RBF_TRY(pool_alloc(&d_c, static_cast<size_t>(cap) * n, p->stream));
+    RBF_TRY(pool_alloc(&d_f, static_cast<size_t>(cap), p->stream));
+    int64_t c = 0;
+    for (int64_t k0 = 0; k0 < N_i && ids_ok; k0 += cap, ++c) {
+      const int b = static_cast<int>(c & 1);
       const int64_t cnt = std::min<int64_t>(cap, N_i - k0);
-      RBF_CK(cudaMemcpyAsync(d_c, rows + k0 * n, sizeof(long long) * cnt * n, cudaMemcpyHostToDevice, p->stream));
+      const int64_t total = cnt * n;
+      RBF_CK(cudaEventSynchronize(sg.ev[b]));  // the previous DMA out of this buffer is done
+      unsigned char* hb = sg.buf[b];
+      int32_t* hc = reinterpret_cast<int32_t*>(hb);
+      double* hf = reinterpret_cast<double*>(hb + ((static_cast<size_t>(total) * 4 + 15) & ~size_t(15)));
+      double* hw = hf + cnt;
+      int bad = 0;
+      const int64_t* src_c = rows + k0 * n;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+      for (int64_t e = 0; e < total; ++e) {
+        const int64_t v = src_c[e];
+        bad |= (v < 0 || v >= N);
+        hc[e] = static_cast<int32_t>(v);
+      }
+      if (bad) {
+        ids_ok = false;
+        break;
+      }
+      std::memcpy(hf, f_int + k0, sizeof(double) * cnt);
+      if (!assemble) {
+        const double* src_w = weights + k0 * n;
+#pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < total; ++e) hw[e] = src_w[e];
+      }
+      RBF_CK(cudaMemcpyAsync(d_c, hc, sizeof(int32_t) * total, cudaMemcpyHostToDevice, p->stream));
+      RBF_CK(cudaMemcpyAsync(d_f, hf, sizeof(double) * cnt, cudaMemcpyHostToDevice, p->stream));
       if (assemble) {  // weights computed on the device, never on the host
         RBF_TRY(launch_assemble(d_pos, d_c, cnt, k0, n, wproto, d_w, d_bad, p->stream));
       } else {
-        RBF_CK(cudaMemcpyAsync(d_w, weights + k0 * n, sizeof(double) * cnt * n, cudaMemcpyHostToDevice, p->stream));
+        RBF_CK(cudaMemcpyAsync(d_w, hw, sizeof(double) * total, cudaMemcpyHostToDevice, p->stream));
       }
-      RBF_CK(cudaMemcpyAsync(d_f, f_int + k0, sizeof(double) * cnt, cudaMemcpyHostToDevice, p->stream));
-      const int64_t total = cnt * n;
+      RBF_CK(cudaEventRecord(sg.ev[b], p->stream));
       const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 32));
       rbf::pack_rows_kernel<<<blocks, 256, 0, p->stream>>>(d_w, d_c, d_f, k0, cnt, n, d_row_of_k,
                                                            p->new_id, N, p->W, p->C, p->F, d_err);
       RBF_CK(cudaGetLastError());
     }
     RBF_CK(cudaStreamSynchronize(p->stream));
-    cudaFree(d_w);
-    cudaFree(d_c);
-    cudaFree(d_f);
+    pool_free(d_w, p->stream);
+    pool_free(d_c, p->stream);
+    pool_free(d_f, p->stream);
+  }
+  if (!ids_ok) {
+    pool_free(d_err, p->stream);
+    pool_free(d_pos, p->stream);
+    pool_free(d_bad, p->stream);
+    rbf_plan_destroy(p.release());
+    return fail(RBF_ERR_PARAM, "stencil node id out of range");
   }
   timer.mark("upload + pack");
   int h_err = 0;
   RBF_CK(cudaMemcpy(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
-  cudaFree(d_err);
+  pool_free(d_err, p->stream);
   if (d_bad) {
     long long bad = 0;
     RBF_CK(cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost));
-    cudaFree(d_bad);
-    cudaFree(d_pos);
+    pool_free(d_bad, p->stream);
+    pool_free(d_pos, p->stream);
     if (bad != std::numeric_limits<long long>::max()) {
       rbf_plan_destroy(p.release());
       return fail(RBF_ERR_PARAM, "degenerate stencil at interior row " + std::to_string(bad));
@@ -703,24 +810,33 @@ int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows
   for (int64_t e = 0; e < N_i * n; ++e)
     if (rows[e] < 0 || rows[e] >= N) return fail(RBF_ERR_PARAM, "stencil node id out of range");
   RBF_CK(cudaSetDevice(device));
+  RBF_TRY(prepare_pool(device));
   cudaStream_t st;
   RBF_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   double* d_pos = nullptr;
-  long long* d_rows = nullptr;
+  int* d_rows = nullptr;
   double* d_w = nullptr;
   long long* d_bad = nullptr;
   const int64_t cap = std::min<int64_t>(N_i, std::max<int64_t>(1, (int64_t(1) << 24) / n));
-  RBF_CK(cudaMalloc(&d_pos, sizeof(double) * 2 * N));
-  RBF_CK(cudaMalloc(&d_rows, sizeof(long long) * cap * n));
-  RBF_CK(cudaMalloc(&d_w, sizeof(double) * cap * n));
-  RBF_CK(cudaMalloc(&d_bad, sizeof(long long)));
   const long long none = std::numeric_limits<long long>::max();
-  RBF_CK(cudaMemcpy(d_bad, &none, sizeof(none), cudaMemcpyHostToDevice));
-  RBF_CK(cudaMemcpy(d_pos, positions, sizeof(double) * 2 * N, cudaMemcpyHostToDevice));
+  std::vector<int32_t> ids(static_cast<size_t>(cap) * n);
   int rc = RBF_OK;
+  if (pool_alloc(&d_pos, static_cast<size_t>(2 * N), st) != RBF_OK ||
+      pool_alloc(&d_rows, static_cast<size_t>(cap) * n, st) != RBF_OK ||
+      pool_alloc(&d_w, static_cast<size_t>(cap) * n, st) != RBF_OK || pool_alloc(&d_bad, 1, st) != RBF_OK)
+    rc = RBF_ERR_CUDA;
+  if (rc == RBF_OK && (cudaMemcpyAsync(d_bad, &none, sizeof(none), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+                       cudaMemcpyAsync(d_pos, positions, sizeof(double) * 2 * N, cudaMemcpyHostToDevice, st) != cudaSuccess))
+    rc = fail(RBF_ERR_CUDA, "upload positions");
   for (int64_t k0 = 0; k0 < N_i && rc == RBF_OK; k0 += cap) {
     const int64_t cnt = std::min<int64_t>(cap, N_i - k0);
-    if (cudaMemcpyAsync(d_rows, rows + k0 * n, sizeof(long long) * cnt * n, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    if (cudaStreamSynchronize(st) != cudaSuccess) {  // `ids` is reused below
+      rc = fail(RBF_ERR_CUDA, "assembly");
+      break;
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < cnt * n; ++e) ids[e] = static_cast<int32_t>(rows[k0 * n + e]);
+    if (cudaMemcpyAsync(d_rows, ids.data(), sizeof(int32_t) * cnt * n, cudaMemcpyHostToDevice, st) != cudaSuccess) {
       rc = fail(RBF_ERR_CUDA, "upload rows");
       break;
     }
@@ -732,10 +848,11 @@ int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows
   if (rc == RBF_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBF_ERR_CUDA, "assembly");
   long long bad = none;
   if (rc == RBF_OK) cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost);
-  cudaFree(d_pos);
-  cudaFree(d_rows);
-  cudaFree(d_w);
-  cudaFree(d_bad);
+  pool_free(d_pos, st);
+  pool_free(d_rows, st);
+  pool_free(d_w, st);
+  pool_free(d_bad, st);
+  cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
   if (rc != RBF_OK) return rc;
   if (bad != none) {
@@ -749,7 +866,7 @@ int rbf_plan_weight_row_sum_max(rbf_plan* p, double* out) {
   if (!p || !out) return fail(RBF_ERR_PARAM, "NULL argument");
   RBF_CK(cudaSetDevice(p->device));
   double* d = nullptr;
-  RBF_CK(cudaMalloc(&d, sizeof(double)));
+  RBF_TRY(pool_alloc(&d, 1, p->stream));
   RBF_CK(cudaMemsetAsync(d, 0, sizeof(double), p->stream));
   const int blocks = static_cast<int>(std::min<int64_t>((p->N_i + 255) / 256, 148 * 8));
   if (p->N_i > 0) {
@@ -758,7 +875,7 @@ int rbf_plan_weight_row_sum_max(rbf_plan* p, double* out) {
   }
   RBF_CK(cudaMemcpyAsync(out, d, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
   RBF_CK(cudaStreamSynchronize(p->stream));
-  cudaFree(d);
+  pool_free(d, p->stream);
   return RBF_OK;
 }
 
@@ -826,10 +943,12 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
   RBF_TRY(normalise_current(p));
   RBF_TRY(reset_status(p, dt, tol));
   int rc;
+  PhaseTimer timer;
   if (p->resident) rc = run_resident(p, limit, steady, copy_back != 0);
   else rc = run_streaming(p, limit, steady, copy_back != 0);
   if (rc != RBF_OK) return rc;
   RBF_CK(cudaStreamSynchronize(p->stream));
+  timer.mark("run total (incl. sync)");
   RBF_TRY(read_status(p));
   float ms = 0.f;
   RBF_CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
@@ -951,17 +1070,19 @@ void rbf_plan_destroy(rbf_plan* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   for (auto& g : p->graphs)
     if (g) cudaGraphExecDestroy(g);
-  cudaFree(p->W);
-  cudaFree(p->C);
-  cudaFree(p->F);
-  cudaFree(p->U[0]);
-  cudaFree(p->U[1]);
-  cudaFree(p->tmp);
-  cudaFree(p->new_id);
-  cudaFree(p->row_of_k);
-  cudaFree(p->halo_send_idx);
-  cudaFree(p->halo_sendbuf);
-  cudaFree(p->st);
+  cudaStream_t s = p->stream;
+  pool_free(p->W, s);
+  pool_free(p->C, s);
+  pool_free(p->F, s);
+  pool_free(p->U[0], s);
+  pool_free(p->U[1], s);
+  pool_free(p->tmp, s);
+  pool_free(p->new_id, s);
+  pool_free(p->row_of_k, s);
+  pool_free(p->halo_send_idx, s);
+  pool_free(p->halo_sendbuf, s);
+  pool_free(p->st, s);
+  if (s) cudaStreamSynchronize(s);
   if (p->h_st) cudaFreeHost(p->h_st);
   if (p->ev0) cudaEventDestroy(p->ev0);
   if (p->ev1) cudaEventDestroy(p->ev1);

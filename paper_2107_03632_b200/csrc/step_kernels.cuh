@@ -323,11 +323,11 @@ __host__ __device__ constexpr int tma_slice_bytes() {
 template <int NJ, int CW, int RPL>
 __global__ void __launch_bounds__(32 * (CW + 1), 1)
 step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeom g) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char tma_smem[];
   constexpr int kMaxStages = 16;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tma_smem);
   uint64_t* empty = full + kMaxStages;
-  unsigned char* ring = smem_raw + 2 * kMaxStages * sizeof(uint64_t);
+  unsigned char* ring = tma_smem + 2 * kMaxStages * sizeof(uint64_t);
   // Chunks issued so far by the producer.  A consumer strides CW units ahead
   // per iteration and can lead the producer by more than one ring lap; an
   // mbarrier parity wait two phases ahead would alias the previous phase, so
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(1024, 1) resident_loop_kernel(ResidentArgs a) 
 // ---- plan construction kernels --------------------------------------------
 // Scatter row-major (reference layout) rows [k0, k0+cnt) into SELL-32 at the
 // renumbered row position; node ids renumbered through new_id.
-__global__ void pack_rows_kernel(const double* __restrict__ w_raw, const long long* __restrict__ c_raw,
+__global__ void pack_rows_kernel(const double* __restrict__ w_raw, const int* __restrict__ c_raw,
                                  const double* __restrict__ f_raw, long long k0, long long cnt, int n,
                                  const long long* __restrict__ row_of_k,  // nullptr: identity
                                  const int* __restrict__ new_id, long long N,
@@ -625,7 +625,7 @@ __global__ void pack_rows_kernel(const double* __restrict__ w_raw, const long lo
     const long long k = k0 + kk;
     const long long r = row_of_k ? row_of_k[k] : k;
     const long long dst = (r >> 5) * static_cast<long long>(n) * 32 + 32LL * j + (r & 31);
-    const long long col = c_raw[e];
+    const long long col = c_raw[e];  // range-checked on the host while staging
     if (col < 0 || col >= N) {
       atomicExch(err, 1);
       continue;

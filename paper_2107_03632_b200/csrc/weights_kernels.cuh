@@ -20,7 +20,7 @@ namespace rbf {
 
 struct WeightArgs {
   const double* pos;       // [N*2] node positions
-  const long long* rows;   // [cnt*n] support node ids (row-major, entry 0 = centre)
+  const int* rows;         // [cnt*n] support node ids (row-major, entry 0 = centre)
   long long cnt;           // rows in this launch
   long long k0;            // global index of the first row (error reporting)
   int n;                   // support size
@@ -47,7 +47,7 @@ __global__ void assemble_weights_kernel(WeightArgs a) {
   double* sy = sx + n;
   for (long long k = static_cast<long long>(blockIdx.x) * nwarps + warp; k < a.cnt;
        k += static_cast<long long>(gridDim.x) * nwarps) {
-    const long long* rk = a.rows + k * n;
+    const int* rk = a.rows + k * n;
     const long long c = rk[0];
     const double cx = a.pos[2 * c], cy = a.pos[2 * c + 1];
     double r2max = 0.0;

@@ -16,6 +16,7 @@ geometry.py:74-86, evaluated in the same order, so they produce the same bits
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -75,10 +76,33 @@ class ShapeStore:
         return self.weights.shape[0]
 
 
-def closed_form_solution(points):
-    """sin(pi x) sin(pi y) -- geometry.py:74-81."""
-    p = np.asarray(points, dtype=float)
+_PAR_MIN = 1 << 18  # points; below this one numpy call is faster
+_PAR_CHUNK = 1 << 16
+
+
+def _closed_form_serial(p):
     return np.sin(np.pi * p[..., 0]) * np.sin(np.pi * p[..., 1])
+
+
+def closed_form_solution(points):
+    """sin(pi x) sin(pi y) -- geometry.py:74-81.
+
+    Large (N, 2) inputs are evaluated in 64 Ki-point chunks on a thread pool
+    (numpy releases the GIL); the expression is elementwise, so every value
+    has the same bits as one call (tests/test_host.py checks it)."""
+    p = np.asarray(points, dtype=float)
+    if p.ndim != 2 or p.shape[0] < _PAR_MIN:
+        return _closed_form_serial(p)
+    out = np.empty(p.shape[0])
+    from concurrent.futures import ThreadPoolExecutor
+
+    def run(lo):
+        hi = min(lo + _PAR_CHUNK, p.shape[0])
+        out[lo:hi] = _closed_form_serial(p[lo:hi])
+
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as pool:
+        list(pool.map(run, range(0, p.shape[0], _PAR_CHUNK)))
+    return out
 
 
 def forcing(points):

@@ -1,0 +1,81 @@
+"""Host-side mirror of the reference solver API (CPU only, no device calls):
+config validation, Dirichlet values, forcing, norms, stability bound -- each
+checked against the reference's expressions / golden values."""
+
+import numpy as np
+import pytest
+
+import paper_2107_03632_b200 as rb
+from paper_2107_03632_b200 import problem
+from oracle import oracle as orc
+
+
+def test_config_validation_mirrors_reference():
+    """test_solver.py:67-79."""
+    with pytest.raises(rb.ParameterError):
+        rb.SolveConfig(nodes=300, h=0.1)
+    with pytest.raises(rb.ParameterError):
+        rb.SolveConfig()
+    with pytest.raises(rb.ParameterError):
+        rb.SolveConfig(nodes=300, dt=-1e-6)
+    with pytest.raises(rb.ParameterError):
+        rb.SolveConfig(nodes=300, steps=-1)
+    with pytest.raises(rb.ParameterError):
+        rb.SolveConfig(nodes=300, mode="implicit")
+    with pytest.raises(rb.ParameterError):
+        rb.SolveConfig(nodes=300, degree=2, support_size=5)
+    cfg = rb.SolveConfig(nodes=300, dt=1e-5, steps=3)
+    assert cfg.as_dict(2e-5)["dt"] == 2e-5 and cfg.as_dict()["m"] == 2
+
+
+def test_errors_are_catchable_as_reference_errors():
+    try:
+        from rbffd import errors as ref  # type: ignore
+    except Exception:
+        pytest.skip("reference package not importable here")
+    assert issubclass(rb.InstabilityError, ref.InstabilityError)
+    assert issubclass(rb.SteadyStateTimeout, ref.SteadyStateTimeout)
+    assert issubclass(rb.ParameterError, ref.ParameterError)
+
+
+@pytest.mark.parametrize("name", ["small", "dome", "m6"])
+def test_host_prep_matches_oracle_bits(golden, manifest, name):
+    nodes, _, shapes, z = golden(name)
+    assert np.array_equal(rb.forcing(nodes.positions), orc.forcing(nodes.positions))
+    u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    assert np.array_equal(u0, orc.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
+    assert rb.stability_bound(shapes) == manifest[name]["stability_bound"]
+    for case, meta in manifest[name].items():
+        if isinstance(meta, dict) and f"{case}__field" in z:
+            assert rb.error_norms(z[f"{case}__field"], nodes) == (meta["linf"], meta["l2"])
+
+
+@pytest.mark.parametrize("n_points", [problem._PAR_MIN, problem._PAR_MIN + 12345, 1_000_003])
+def test_parallel_closed_form_is_bitwise(n_points):
+    rng = np.random.default_rng(n_points)
+    pts = rng.uniform(-1, 1, (n_points, 2))
+    assert np.array_equal(problem.closed_form_solution(pts), problem._closed_form_serial(pts))
+    assert np.array_equal(rb.forcing(pts), 2.0 * np.pi**2 * problem._closed_form_serial(pts))
+
+
+def test_interior_rows_view_matches_gather():
+    from paper_2107_03632_b200.solver import _interior_rows
+
+    nb = np.arange(40, dtype=np.int64).reshape(10, 4)
+    assert np.array_equal(_interior_rows(nb, np.arange(3, 10)), nb[np.arange(3, 10)])
+    perm = np.array([9, 3, 5])
+    assert np.array_equal(_interior_rows(nb, perm), nb[perm])
+
+
+def test_synthetic_domain_shape():
+    from paper_2107_03632_b200 import synth
+
+    nodes, st, sh = synth.synthetic_problem(5000, 15, 2, seed=2)
+    assert abs(nodes.n_total - 5000) < 150
+    assert np.array_equal(sh.interior_nodes, np.arange(nodes.n_boundary, nodes.n_total))
+    assert np.array_equal(st.neighbors[:, 0], np.arange(nodes.n_total))
+    assert np.all(np.hypot(*nodes.positions[nodes.is_boundary].T) == pytest.approx(1.0))
+    # Laplacian weights reproduce x^2 + y^2 -> 4 on every row
+    rows = st.neighbors[sh.interior_nodes]
+    vals = (nodes.positions[:, 0] ** 2 + nodes.positions[:, 1] ** 2)[rows]
+    assert np.allclose(np.einsum("ij,ij->i", sh.weights, vals), 4.0, rtol=1e-6)
