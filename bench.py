@@ -3,7 +3,7 @@
 node-updates/s, and the fraction of the HBM roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c1|c3|c4] [--native] [--ldg] [--quick]
+                    [--workload c2|c1|c3|c4|c2x10] [--native] [--ldg] [--quick]
 
 One bench "step" is one pseudo-time iteration over every interior row (one
 pass of the hot path, solver.py:198-217); a node-update is one interior row in
@@ -42,6 +42,7 @@ WORKLOADS = {
     "c1": (1027, 15, 2, "C1: paper Fig. 1 case, m=2 n=15 N=1027 (golden fixture, reference nodes)"),
     "c2": (1_000_000, 15, 2, "C2: m=2 n=15 N=1e6 synthetic scattered disk, fp64, 1xB200"),
     "c3": (10_000_000, 30, 4, "C3: m=4 n=30 N=1e7 synthetic scattered disk, fp64, 1xB200"),
+    "c2x10": (10_000_000, 15, 2, "m=2 n=15 N=1e7 synthetic scattered disk, fp64, 1xB200 (north-star m=2 at N>=1e7)"),
     "c4": (25_000_000, 56, 6, "C4: m=6 n=56 N=2.5e7 synthetic scattered disk, fp64, 1xB200"),
 }
 
