@@ -51,6 +51,7 @@ extern "C" {
 #define RBF_NO_RESIDENT 0x2u      /* never use the on-chip (single-CTA) resident loop */
 #define RBF_NO_PDL 0x4u           /* disable programmatic dependent launch between steps */
 #define RBF_STREAM_LDG 0x8u       /* streaming step with plain loads instead of the TMA ring */
+#define RBF_NO_CLUSTER 0x10u      /* small problems: single-CTA resident loop, not the cluster loop */
 
 /* run modes (SolveConfig.mode, solver.py:53) */
 #define RBF_MODE_FIXED 0
@@ -159,7 +160,8 @@ typedef struct rbf_plan_info {
   int32_t renumbered;      /* 1: rows/nodes permuted (field order restored on get/set) */
   int32_t kernel_n;        /* compile-time width of the chosen step kernel (0: generic) */
   int32_t grid, block;     /* streaming kernel launch geometry */
-  int32_t variant;         /* 0 resident loop, 1 LDG streaming step, 2 TMA-ring streaming step */
+  int32_t variant;         /* 0 resident loop (1 CTA), 1 LDG streaming step, 2 TMA-ring
+                              streaming step, 3 cluster-resident loop (DSMEM halo) */
   int64_t device_bytes;    /* device memory held by the plan */
   int64_t bytes_per_step;  /* algorithmic HBM bytes per step: N_i*(12n+24) */
   int64_t launches;        /* kernel launches issued by this plan so far */

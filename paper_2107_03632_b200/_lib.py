@@ -24,6 +24,7 @@ RBF_RENUMBER_MORTON = 0x1
 RBF_NO_RESIDENT = 0x2
 RBF_NO_PDL = 0x4
 RBF_STREAM_LDG = 0x8
+RBF_NO_CLUSTER = 0x10
 
 RBF_MODE_FIXED = 0
 RBF_MODE_STEADY = 1

@@ -63,11 +63,13 @@ constexpr size_t kResidentSmemMax = 227 * 1024;
 using StreamFn = void (*)(rbf::StepArgs, const double*, double*, int);
 using TmaFn = void (*)(rbf::StepArgs, const double*, double*, int, rbf::TmaGeom);
 using ResidentFn = void (*)(rbf::ResidentArgs);
+using ClusterFn = void (*)(rbf::ClusterArgs);
 
 template <int NJ>
 struct KernelSet {
   static StreamFn stream() { return rbf::step_stream_kernel<NJ>; }
   static ResidentFn resident() { return rbf::resident_loop_kernel<NJ>; }
+  static ClusterFn cluster() { return rbf::cluster_loop_kernel<NJ>; }
   // consumer warps: 15 (512-thread CTA, <=128 regs) for narrow stencils, 8
   // (<=168 regs) for wide ones whose NJ gathers need the registers
   static constexpr int kCW = NJ <= 32 ? 15 : 8;
@@ -166,7 +168,11 @@ struct rbf_plan {
   rbf::TmaGeom tma_geom = {1, 2};
   size_t tma_smem = 0;
   int tma_block = 0;
-  int variant = 1;                 // 0 resident, 1 LDG streaming, 2 TMA streaming
+  int variant = 1;                 // 0 resident, 1 LDG streaming, 2 TMA streaming, 3 cluster loop
+  ClusterFn cluster_fn = nullptr;  // non-null: the loop runs in one thread-block cluster
+  int cluster_q = 0, cluster_rpc = 0, cluster_threads = 0;
+  size_t cluster_smem = 0;
+  unsigned int* cluster_dest = nullptr;
   int kernel_n = 0;
   bool resident = false;
   size_t resident_smem = 0;
@@ -431,7 +437,39 @@ int run_streaming(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
 
 int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
   RBF_CK(cudaEventRecord(p->ev0, p->stream));
-  if (limit > 0 && p->N_i > 0) {
+  if (limit > 0 && p->N_i > 0 && p->cluster_fn) {
+    // buffer discipline makes copy-back and swap value-identical;
+    // the cluster loop always swaps
+    rbf::ClusterArgs a;
+    a.W = p->W;
+    a.C = p->C;
+    a.F = p->F;
+    a.dest = p->cluster_dest;
+    a.U0 = p->U[0];
+    a.U1 = p->U[1];
+    a.n_rows = p->N_i;
+    a.N = p->N;
+    a.dst_base = p->B;
+    a.limit = limit;
+    a.n = p->n;
+    a.flags = steady ? rbf::kSteady : 0;
+    a.rpc = p->cluster_rpc;
+    a.st = p->st;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p->cluster_q);
+    cfg.blockDim = dim3(p->cluster_threads);
+    cfg.dynamicSmemBytes = p->cluster_smem;
+    cfg.stream = p->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p->cluster_q;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RBF_CK(cudaLaunchKernelEx(&cfg, p->cluster_fn, a));
+    ++p->launches;
+  } else if (limit > 0 && p->N_i > 0) {
     rbf::ResidentArgs a;
     a.W = p->W;
     a.C = p->C;
@@ -738,9 +776,60 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
       cudaGetLastError();
     }
   }
+  // cluster-resident loop: rows spread over Q SMs of one cluster (DSMEM halo)
+  if (!(flags & RBF_NO_RESIDENT) && !(flags & RBF_NO_CLUSTER) && N_i >= 256) {
+    int q = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(2, (N_i + 63) / 64)));
+    if (const char* e = std::getenv("RBFFD_CLUSTER")) q = std::max(2, std::min(16, std::atoi(e)));
+    const int rpc = static_cast<int>(((N_i + q - 1) / q + 1) & ~int64_t(1));
+    const int rp = rpc;
+    const size_t NU = static_cast<size_t>(((B + 1) & ~int64_t(1)) + N_i + 2);
+    const size_t csmem = 2 * NU * 8 + 2 * 16 * 2 * 8 + static_cast<size_t>(n) * rp * 12 + rp * 8 + rp * 4;
+    ClusterFn cfn = nullptr;
+    switch (n) {
+#define RBF_CCASE(K) \
+  case K:            \
+    cfn = KernelSet<K>::cluster(); \
+    break;
+      RBF_SPECIALISED(RBF_CCASE)
+#undef RBF_CCASE
+      default:
+        cfn = KernelSet<0>::cluster();
+    }
+    const int threads = std::min(1024, ((rpc + 31) / 32) * 32);
+    if (csmem <= 200 * 1024 &&
+        cudaFuncSetAttribute(cfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(csmem)) == cudaSuccess &&
+        (q <= 8 || cudaFuncSetAttribute(cfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(q);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = csmem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = q;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, cfn, &cfg) == cudaSuccess && nclusters >= 1) {
+        RBF_TRY(dev_alloc(p.get(), &p->cluster_dest, static_cast<size_t>(N_i)));
+        RBF_CK(cudaMemsetAsync(p->cluster_dest, 0, sizeof(unsigned int) * N_i, p->stream));
+        const int blocks = static_cast<int>(std::min<int64_t>((N_i * n + 255) / 256, 148 * 16));
+        rbf::cluster_dest_kernel<<<blocks, 256, 0, p->stream>>>(p->C, N_i, n, B, rpc, p->cluster_dest);
+        RBF_CK(cudaGetLastError());
+        p->cluster_fn = cfn;
+        p->cluster_q = q;
+        p->cluster_rpc = rpc;
+        p->cluster_threads = threads;
+        p->cluster_smem = csmem;
+        p->resident = true;
+      }
+    }
+    cudaGetLastError();
+  }
   int sms = 148, per_sm = 1;
   RBF_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  p->variant = p->resident ? 0 : 1;
+  p->variant = p->cluster_fn ? 3 : (p->resident ? 0 : 1);
   if (tma_fn && !(flags & RBF_STREAM_LDG) && N_i > 0) {
     // ring geometry: ~24 KB stages, as many as fit in ~200 KB of shared memory
     const int slice = n * 32 * 12 + 32 * 8;
@@ -762,7 +851,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
       int occ = 1;
       RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tma_fn, p->tma_block, smem_t));
       p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(chunks, int64_t(sms) * std::max(occ, 1))));
-      if (!p->resident) p->variant = 2;
+      if (!p->resident && !p->cluster_fn) p->variant = 2;
     } else {
       cudaGetLastError();
     }
@@ -973,7 +1062,7 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
   if (s.bad_step >= 0) {
     // field of the failing step's u2 (solver.py:201)
     p->cur = copy_back ? 0 : static_cast<int>((s.bad_step + 1) & 1);
-    if (p->resident) p->cur = 0;
+    if (p->resident) p->cur = 0;  // resident / cluster loops publish into both buffers
     if (steps_done) *steps_done = s.bad_step;
     if (has_residual) *has_residual = 0;
     return fail(RBF_ERR_INSTABILITY, "time loop unstable at step " + std::to_string(s.bad_step));
@@ -1080,6 +1169,7 @@ void rbf_plan_destroy(rbf_plan* p) {
   pool_free(p->new_id, s);
   pool_free(p->row_of_k, s);
   pool_free(p->halo_send_idx, s);
+  pool_free(p->cluster_dest, s);
   pool_free(p->halo_sendbuf, s);
   pool_free(p->st, s);
   if (s) cudaStreamSynchronize(s);

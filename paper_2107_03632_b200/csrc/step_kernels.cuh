@@ -22,6 +22,7 @@
 // bytes: 8n (W) + 4n (C) + 8 (F) + 8 (u_self) + 8 (u write) = 12n + 24.
 #pragma once
 #include <cstdint>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 namespace rbf {
@@ -605,6 +606,196 @@ __global__ void __launch_bounds__(1024, 1) resident_loop_kernel(ResidentArgs a) 
     st->last_res_bits = last_bits;
     st->last_res_step = last_res_step;
     st->step = (bad_step >= 0) ? bad_step + 1 : step;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cluster-resident loop: the small-problem loop spread over a thread-block
+// cluster of Q CTAs (Q <= 16, one SM each) instead of one SM.  Every CTA keeps
+// the whole field (double-buffered) and its own rows' weights / ids / forcing
+// in shared memory; per step it updates its rows and pushes each new value
+// straight into the shared memory of the CTAs whose stencils read it (DSMEM
+// stores, per-row destination masks built on the host), plus its partial
+// residual max / non-finite flag into every CTA's reduction slots; one
+// cluster barrier (release / acquire) then publishes the step.  All CTAs take
+// the same stop decision from the same reduced values (solver.py:200-217).
+struct ClusterArgs {
+  const double* W;          // SELL-32 (plan layout), rows of all CTAs
+  const int* C;
+  const double* F;
+  const unsigned int* dest;    // [N_i] bit q: CTA q (other than the owner) reads this row's node
+  double* U0;               // global field buffers (start field in U0)
+  double* U1;
+  long long n_rows, N, dst_base, limit;
+  int n, flags, rpc;        // rows per CTA (even)
+  DevStatus* st;
+};
+
+template <int NJ>
+__global__ void __launch_bounds__(1024, 1) cluster_loop_kernel(ClusterArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char cl_smem[];
+  const int n = NJ > 0 ? NJ : a.n;
+  const int q = static_cast<int>(cluster.block_rank());
+  const int Q = static_cast<int>(cluster.num_blocks());
+  const int B = static_cast<int>(a.dst_base);
+  const int IB = (B + 1) & ~1;             // interior rows start 16-B aligned
+  const int NU = IB + static_cast<int>(a.n_rows) + 2;
+  const int r0 = q * a.rpc;
+  const int r1 = min(static_cast<int>(a.n_rows), r0 + a.rpc);
+  const int nr = max(0, r1 - r0);
+  const int rp = (a.rpc + 1) & ~1;
+  // smem: U[2][NU] | red[2][16][2] u64 | W[n][rp] | F[rp] | C[n][rp] | mask[rp] (u32)
+  double* U = reinterpret_cast<double*>(cl_smem);
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(U + 2 * NU);
+  double* sW = reinterpret_cast<double*>(red + 2 * 16 * 2);
+  double* sF = sW + static_cast<size_t>(n) * rp;
+  int* sC = reinterpret_cast<int*>(sF + rp);
+  unsigned int* sM = reinterpret_cast<unsigned int*>(sC + static_cast<size_t>(n) * rp);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = (nt + 31) >> 5;
+  __shared__ unsigned long long s_part[32][2];
+
+  for (int i = tid; i < static_cast<int>(a.N); i += nt) {
+    const int li = i < B ? i : i - B + IB;
+    const double v = a.U0[i];
+    U[li] = v;
+    U[NU + li] = v;
+  }
+  for (int k = tid; k < nr; k += nt) {
+    const int r = r0 + k;
+    const long long base = (r >> 5) * static_cast<long long>(n) * 32 + (r & 31);
+    for (int j = 0; j < n; ++j) {
+      sW[j * rp + k] = a.W[base + 32LL * j];
+      const int c = a.C[base + 32LL * j];
+      sC[j * rp + k] = c < B ? c : c - B + IB;
+    }
+    sF[k] = a.F[r];
+    sM[k] = a.dest[r];
+  }
+  for (int i = tid; i < 2 * 16 * 2; i += nt) red[i] = 0ull;
+  cluster.sync();
+
+  DevStatus* st = a.st;
+  const double dt = st->dt, tol = st->tol;
+  const bool steady = (a.flags & kSteady) != 0;
+  long long step = 0, bad_step = -1, conv_step = -1, last_res_step = -1;
+  unsigned long long last_bits = 0;
+  int cur = 0;
+  for (; step < a.limit; ++step) {
+    const int nxt = cur ^ 1;
+    const bool need_res = steady || step == a.limit - 1;
+    const double* uc = U + cur * NU;
+    double* un = U + nxt * NU;
+    bool bad = false;
+    unsigned long long dmax = 0ull;
+    for (int k = tid; k < nr; k += nt) {
+      double acc = 0.0;
+      if constexpr (NJ > 0) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(sW[j * rp + k], uc[sC[j * rp + k]]));
+      } else {
+        for (int j = 0; j < n; ++j) acc = __dadd_rn(acc, __dmul_rn(sW[j * rp + k], uc[sC[j * rp + k]]));
+      }
+      const int li = IB + r0 + k;
+      const double u_self = uc[li];
+      const double value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(sF[k], acc)));
+      un[li] = value;
+      unsigned int m = sM[k];
+      while (m) {  // push to the CTAs that read this node
+        const int dq = __ffs(m) - 1;
+        m &= m - 1;
+        *cluster.map_shared_rank(un + li, dq) = value;
+      }
+      bad |= !isfinite(value);
+      if (need_res) {
+        const unsigned long long b =
+            static_cast<unsigned long long>(__double_as_longlong(fabs(__dsub_rn(value, u_self))));
+        dmax = b > dmax ? b : dmax;
+      }
+    }
+    // CTA partials -> every CTA's slot [nxt][q]
+    unsigned long long wm = warp_max_u64(dmax);
+    const unsigned int wb = __any_sync(0xffffffffu, bad) ? 1u : 0u;
+    if (lane == 0) {
+      s_part[warp][0] = wm;
+      s_part[warp][1] = wb;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long m0 = 0, m1 = 0;
+      for (int w = 0; w < nwarps; ++w) {
+        m0 = s_part[w][0] > m0 ? s_part[w][0] : m0;
+        m1 |= s_part[w][1];
+      }
+      for (int dq = 0; dq < Q; ++dq) {
+        unsigned long long* slot = cluster.map_shared_rank(red + (nxt * 16 + q) * 2, dq);
+        slot[0] = m0;
+        slot[1] = m1;
+      }
+    }
+    cluster.sync();  // publishes the step: field values and partials
+    unsigned long long gmax = 0ull, gbad = 0ull;
+    for (int dq = 0; dq < Q; ++dq) {
+      const unsigned long long* slot = red + (nxt * 16 + dq) * 2;
+      gmax = slot[0] > gmax ? slot[0] : gmax;
+      gbad |= slot[1];
+    }
+    cur = nxt;
+    if (gbad) {
+      bad_step = step;
+      break;
+    }
+    if (need_res) {
+      last_bits = gmax;
+      last_res_step = step;
+      if (steady && __ddiv_rn(__longlong_as_double(static_cast<long long>(gmax)), dt) <= tol) {
+        conv_step = step;
+        ++step;
+        break;
+      }
+    }
+  }
+  // the field after the last executed step (after a failure: its u2) is U[cur]
+  const double* uf = U + cur * NU;
+  for (int k = tid; k < nr; k += nt) {
+    const long long node = a.dst_base + r0 + k;
+    const double v = uf[IB + r0 + k];
+    a.U0[node] = v;
+    a.U1[node] = v;
+  }
+  if (q == 0) {
+    for (int i = tid; i < B; i += nt) {
+      a.U0[i] = uf[i];
+      a.U1[i] = uf[i];
+    }
+    if (tid == 0) {
+      st->bad_step = bad_step;
+      st->conv_step = conv_step;
+      st->last_res_bits = last_bits;
+      st->last_res_step = last_res_step;
+      st->step = (bad_step >= 0) ? bad_step + 1 : step;
+    }
+  }
+  cluster.sync();  // no CTA leaves while a peer may still address its shared memory
+}
+
+// dest[row(c)] |= 1 << owner(r) for every stencil entry c of row r that is an
+// interior node owned by another CTA of the cluster (owner(r) = r / rpc)
+__global__ void cluster_dest_kernel(const int* __restrict__ C, long long n_rows, int n, long long B,
+                                    int rpc, unsigned int* __restrict__ dest) {
+  const long long total = n_rows * n;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = e / n;
+    const int j = static_cast<int>(e - r * n);
+    const long long base = (r >> 5) * static_cast<long long>(n) * 32 + (r & 31);
+    const long long c = C[base + 32LL * j];
+    if (c < B) continue;
+    const long long rc = c - B;
+    const int qr = static_cast<int>(r / rpc), qc = static_cast<int>(rc / rpc);
+    if (qr != qc) atomicOr(dest + rc, 1u << qr);
   }
 }
 

@@ -52,6 +52,28 @@ def check_report(rep, meta, field):
     assert rep.config["dt"] == meta["dt"]
 
 
+@pytest.mark.parametrize("name,case", [("small", "steady"), ("crit6", "fixed100"), ("m4", "fixed200"),
+                                       ("m6", "fixed100"), ("dome", "steady"), ("small", "fixed120")])
+@pytest.mark.parametrize("q", ["2", "5", "8", "16"])
+def test_cluster_loop_sizes_match_reference(golden, manifest, name, case, q, monkeypatch):
+    """Cluster-resident loop for 2..16 CTAs per cluster (RBFFD_CLUSTER)."""
+    monkeypatch.setenv("RBFFD_CLUSTER", q)
+    nodes, _, shapes, z = golden(name)
+    meta = manifest[name][case]
+    interior = shapes.interior_nodes
+    plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                rb.forcing(nodes.positions[interior]))
+    info = plan.info()
+    if info["variant"] != 3:
+        pytest.skip(f"{name} does not fit the cluster loop")
+    plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
+    res = plan.run(meta["dt"], steps=meta["config_steps"], mode=meta["mode"], tol=meta["tol"],
+                   max_steps=meta["max_steps"])
+    assert res.steps_done == meta["steps"] and res.residual == meta["residual"]
+    assert np.array_equal(plan.get_field(), z[f"{case}__field"])
+    plan.close()
+
+
 @pytest.mark.parametrize("renumber", [False, True], ids=["native", "morton"])
 @pytest.mark.parametrize("name,case", CASES)
 def test_run_time_loop_matches_reference(golden, manifest, name, case, renumber):
@@ -64,21 +86,22 @@ def test_run_time_loop_matches_reference(golden, manifest, name, case, renumber)
 
 @pytest.mark.parametrize("case", ["paper", "steady"])
 def test_streaming_loop_matches_resident_loop(golden, manifest, case):
-    """The Fig. 1 case normally runs on-chip in one CTA; force the streaming
-    graph/PDL path (and its fused steady-state stop) and demand the same bits."""
+    """The Fig. 1 case normally runs on-chip (cluster loop); force the
+    single-CTA loop and the streaming graph/PDL paths (and their fused
+    steady-state stop) and demand the same bits from every one."""
     nodes, _, shapes, z = golden("dome")
     meta = manifest["dome"][case]
     interior = shapes.interior_nodes
     rows = shapes.stencils.neighbors[interior]
     f_int = rb.forcing(nodes.positions[interior])
     u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
-    for resident, pdl, tma in ((True, True, True), (False, True, True), (False, False, True),
-                               (False, True, False), (False, False, False)):
+    for resident, cluster, pdl, tma, variant in (
+            (True, True, True, True, 3), (True, False, True, True, 0), (False, True, True, True, 2),
+            (False, True, False, True, 2), (False, True, True, False, 1), (False, True, False, False, 1)):
         plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, resident=resident,
-                    pdl=pdl, tma=tma)
+                    pdl=pdl, tma=tma, cluster=cluster)
         info = plan.info()
-        assert info["resident"] == int(resident)
-        assert info["variant"] == (0 if resident else (2 if tma else 1))
+        assert info["variant"] == variant
         plan.set_field(u0)
         res = plan.run(meta["dt"], steps=meta["config_steps"], mode=meta["mode"], tol=meta["tol"],
                        max_steps=meta["max_steps"])
