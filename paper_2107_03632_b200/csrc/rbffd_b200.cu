@@ -133,6 +133,15 @@ struct PhaseTimer {
   }
 };
 
+// The dynamic shared-memory cap is per-function global state: raise it once to
+// the device maximum (never to a plan's own size, or a later, smaller plan
+// would invalidate the launches of an earlier, larger one).
+template <typename F>
+cudaError_t set_max_smem(F fn) {
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(kResidentSmemMax));
+}
+
 uint64_t morton2(uint32_t x, uint32_t y) {
   auto spread = [](uint64_t v) {
     v &= 0x1fffffull;
@@ -537,8 +546,7 @@ int launch_assemble(const double* d_pos, const int* d_rows, long long cnt, long 
   int warps = static_cast<int>(std::min<size_t>(8, (200 * 1024) / per_warp));
   if (warps < 1) return fail(RBF_ERR_PARAM, "support too large for on-chip weight assembly");
   const size_t smem = per_warp * warps;
-  RBF_CK(cudaFuncSetAttribute(rbf::assemble_weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(smem)));
+  RBF_CK(set_max_smem(rbf::assemble_weights_kernel));
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const long long blocks = std::min<long long>((cnt + warps - 1) / warps, static_cast<long long>(sms) * 8);
@@ -768,8 +776,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
                       static_cast<size_t>(rows_pad) * sizeof(double) +
                       2 * static_cast<size_t>(N) * sizeof(double);
   if (!(flags & RBF_NO_RESIDENT) && N_i > 0 && smem <= kResidentSmemMax - 1024) {
-    if (cudaFuncSetAttribute(p->resident_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem)) == cudaSuccess) {
+    if (set_max_smem(p->resident_fn) == cudaSuccess) {
       p->resident = true;
       p->resident_smem = smem;
     } else {
@@ -797,7 +804,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
     }
     const int threads = std::min(1024, ((rpc + 31) / 32) * 32);
     if (csmem <= 200 * 1024 &&
-        cudaFuncSetAttribute(cfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(csmem)) == cudaSuccess &&
+        set_max_smem(cfn) == cudaSuccess &&
         (q <= 8 || cudaFuncSetAttribute(cfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(q);
@@ -840,9 +847,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
     int stages = std::max(2, std::min(8, static_cast<int>((200 * 1024) / stage)));
     if (const char* e = std::getenv("RBFFD_TMA_STAGES")) stages = std::max(2, std::min(16, std::atoi(e)));
     const size_t smem_t = 2 * 16 * sizeof(uint64_t) + static_cast<size_t>(stages) * stage;
-    if (smem_t <= kResidentSmemMax &&
-        cudaFuncSetAttribute(tma_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem_t)) == cudaSuccess) {
+    if (smem_t <= kResidentSmemMax && set_max_smem(tma_fn) == cudaSuccess) {
       p->tma_fn = tma_fn;
       p->tma_geom = rbf::TmaGeom{sps, stages};
       p->tma_smem = smem_t;

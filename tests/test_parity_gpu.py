@@ -74,6 +74,24 @@ def test_cluster_loop_sizes_match_reference(golden, manifest, name, case, q, mon
     plan.close()
 
 
+def test_interleaved_plans_of_different_sizes(golden, manifest):
+    """Kernel attributes are process-global: building a smaller plan must not
+    break launches of an earlier, larger one (each loop kind)."""
+    runs = []
+    for name, case in (("m6", "fixed100"), ("crit6", "fixed100"), ("dome", "paper"), ("small", "fixed50")):
+        nodes, _, shapes, z = golden(name)
+        interior = shapes.interior_nodes
+        for kw in (dict(), dict(cluster=False), dict(resident=False)):
+            plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                        rb.forcing(nodes.positions[interior]), **kw)
+            runs.append((plan, nodes, manifest[name][case], z[f"{case}__field"]))
+    for plan, nodes, meta, field in reversed(runs):
+        plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
+        res = plan.run(meta["dt"], steps=meta["config_steps"])
+        assert res.residual == meta["residual"]
+        assert np.array_equal(plan.get_field(), field)
+
+
 @pytest.mark.parametrize("renumber", [False, True], ids=["native", "morton"])
 @pytest.mark.parametrize("name,case", CASES)
 def test_run_time_loop_matches_reference(golden, manifest, name, case, renumber):
