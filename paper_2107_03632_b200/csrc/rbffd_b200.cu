@@ -138,8 +138,15 @@ struct PhaseTimer {
 // would invalidate the launches of an earlier, larger one).
 template <typename F>
 cudaError_t set_max_smem(F fn) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(kResidentSmemMax));
+                              optin - static_cast<int>(fa.sharedSizeBytes));
 }
 
 uint64_t morton2(uint32_t x, uint32_t y) {
