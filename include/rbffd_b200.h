@@ -52,6 +52,7 @@ extern "C" {
 #define RBF_NO_PDL 0x4u           /* disable programmatic dependent launch between steps */
 #define RBF_STREAM_LDG 0x8u       /* streaming step with plain loads instead of the TMA ring */
 #define RBF_NO_CLUSTER 0x10u      /* small problems: single-CTA resident loop, not the cluster loop */
+#define RBF_NO_IDX16 0x20u        /* keep int32 node ids in the streamed step (no 16-bit windows) */
 
 /* run modes (SolveConfig.mode, solver.py:53) */
 #define RBF_MODE_FIXED 0
@@ -162,9 +163,11 @@ typedef struct rbf_plan_info {
   int32_t grid, block;     /* streaming kernel launch geometry */
   int32_t variant;         /* 0 resident loop (1 CTA), 1 LDG streaming step, 2 TMA-ring
                               streaming step, 3 cluster-resident loop (DSMEM halo) */
+  int32_t index_bits;      /* 32, or 16: two-window 16-bit ids streamed by the TMA step */
   int64_t device_bytes;    /* device memory held by the plan */
   int64_t bytes_per_step;  /* algorithmic HBM bytes per step: N_i*(12n+24) */
   int64_t launches;        /* kernel launches issued by this plan so far */
+  int64_t stream_bytes_per_step; /* bytes the step actually streams (<= bytes_per_step with 16-bit ids) */
 } rbf_plan_info;
 
 int rbf_plan_get_info(const rbf_plan* plan, rbf_plan_info* info);

@@ -25,6 +25,7 @@ RBF_NO_RESIDENT = 0x2
 RBF_NO_PDL = 0x4
 RBF_STREAM_LDG = 0x8
 RBF_NO_CLUSTER = 0x10
+RBF_NO_IDX16 = 0x20
 
 RBF_MODE_FIXED = 0
 RBF_MODE_STEADY = 1
@@ -66,9 +67,11 @@ class PlanInfo(ctypes.Structure):
         ("grid", ctypes.c_int32),
         ("block", ctypes.c_int32),
         ("variant", ctypes.c_int32),
+        ("index_bits", ctypes.c_int32),
         ("device_bytes", ctypes.c_int64),
         ("bytes_per_step", ctypes.c_int64),
         ("launches", ctypes.c_int64),
+        ("stream_bytes_per_step", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

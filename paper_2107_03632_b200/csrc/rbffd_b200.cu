@@ -73,15 +73,16 @@ struct KernelSet {
   // consumer warps: 15 (512-thread CTA, <=128 regs) for narrow stencils, 8
   // (<=168 regs) for wide ones whose NJ gathers need the registers
   static constexpr int kCW = NJ <= 32 ? 15 : 8;
-  static TmaFn tma(int rpl_req) {
+  static TmaFn tma(int rpl_req, bool idx16) {
     if constexpr (NJ > 0) {
       // two rows per lane measured slower on B200 (profiles/); opt-in only
       if constexpr (NJ <= 20) {
-        if (rpl_req == 2) return rbf::step_tma_kernel<NJ, kCW, 2>;
+        if (rpl_req == 2) return rbf::step_tma_kernel<NJ, kCW, 2, 4>;
       }
-      return rbf::step_tma_kernel<NJ, kCW, 1>;
+      return idx16 ? rbf::step_tma_kernel<NJ, kCW, 1, 2> : rbf::step_tma_kernel<NJ, kCW, 1, 4>;
     } else {
       (void)rpl_req;
+      (void)idx16;
       return nullptr;
     }
   }
@@ -95,14 +96,14 @@ struct KernelSet {
   X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(12) X(15) X(16) X(20) X(21) X(24) X(28) X(30) X(32) \
   X(36) X(40) X(42) X(45) X(48) X(56) X(60) X(64)
 
-bool pick_kernels(int n, int rpl_req, StreamFn* s, ResidentFn* r, TmaFn* t, int* kn, int* rpl,
-                  int* cw) {
+bool pick_kernels(int n, int rpl_req, bool idx16, StreamFn* s, ResidentFn* r, TmaFn* t, int* kn,
+                  int* rpl, int* cw) {
   switch (n) {
 #define RBF_CASE(K)                        \
   case K:                                  \
     *s = KernelSet<K>::stream();           \
     *r = KernelSet<K>::resident();         \
-    *t = KernelSet<K>::tma(rpl_req);       \
+    *t = KernelSet<K>::tma(rpl_req, idx16); \
     *rpl = KernelSet<K>::rpl(rpl_req);     \
     *cw = KernelSet<K>::cw();              \
     *kn = K;                               \
@@ -189,6 +190,10 @@ struct rbf_plan {
   int cluster_q = 0, cluster_rpc = 0, cluster_threads = 0;
   size_t cluster_smem = 0;
   unsigned int* cluster_dest = nullptr;
+  unsigned short* C16 = nullptr;   // 16-bit two-window ids (index_bits == 16)
+  int4* meta = nullptr;            // per-slice {base0, base1, ok, 0}
+  int index_bits = 32;
+  int64_t overflow_slices = 0;
   int kernel_n = 0;
   bool resident = false;
   size_t resident_smem = 0;
@@ -216,6 +221,8 @@ struct rbf_plan {
     a.dst_base = B;
     a.n = n;
     a.st = st;
+    a.C16 = C16;
+    a.meta = meta;
     return a;
   }
 };
@@ -777,7 +784,44 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   if (const char* e = std::getenv("RBFFD_TMA_RPL")) rpl_req = std::atoi(e);
   TmaFn tma_fn = nullptr;
   int rpl = 1;
-  pick_kernels(n, rpl_req, &p->stream_fn, &p->resident_fn, &tma_fn, &p->kernel_n, &rpl, &cw);
+  // 16-bit two-window ids for the TMA ring (only worth it when almost every
+  // slice fits; the rest fall back to int32 ids read from HBM)
+  bool idx16 = false;
+  {
+    StreamFn sf;
+    ResidentFn rf;
+    TmaFn tf = nullptr;
+    int kn, r1, c1;
+    pick_kernels(n, 1, false, &sf, &rf, &tf, &kn, &r1, &c1);
+    const char* e = std::getenv("RBFFD_IDX16");
+    if (tf && N_i >= 4096 && !(flags & RBF_NO_IDX16) && !(flags & RBF_STREAM_LDG) &&
+        !(e && std::atoi(e) == 0)) {
+      RBF_TRY(dev_alloc(p.get(), &p->C16, sell));
+      RBF_TRY(dev_alloc(p.get(), &p->meta, static_cast<size_t>(p->S)));
+      unsigned long long* d_over = nullptr;
+      RBF_TRY(pool_alloc(&d_over, 1, p->stream));
+      RBF_CK(cudaMemsetAsync(d_over, 0, sizeof(unsigned long long), p->stream));
+      const int blocks = static_cast<int>(std::min<int64_t>((p->S * 32 + 255) / 256, 148 * 16));
+      rbf::compress_ids_kernel<<<blocks, 256, 0, p->stream>>>(p->C, N_i, n, p->C16, p->meta, d_over);
+      RBF_CK(cudaGetLastError());
+      unsigned long long over = 0;
+      RBF_CK(cudaMemcpyAsync(&over, d_over, sizeof(over), cudaMemcpyDeviceToHost, p->stream));
+      RBF_CK(cudaStreamSynchronize(p->stream));
+      pool_free(d_over, p->stream);
+      const bool force = e && std::atoi(e) == 2;  // tests: exercise the overflow path
+      if (force || over * 20 <= static_cast<unsigned long long>(p->S)) {  // <= 5 % of the slices overflow
+        idx16 = true;
+        p->overflow_slices = static_cast<int64_t>(over);
+      } else {
+        pool_free(p->C16, p->stream);
+        pool_free(p->meta, p->stream);
+        p->device_bytes -= static_cast<int64_t>(sell * sizeof(unsigned short) + p->S * sizeof(int4));
+      }
+    }
+  }
+  pick_kernels(n, rpl_req, idx16 && rpl_req != 2, &p->stream_fn, &p->resident_fn, &tma_fn, &p->kernel_n,
+               &rpl, &cw);
+  p->index_bits = (idx16 && rpl_req != 2) ? 16 : 32;
   const int64_t rows_pad = ((N_i + 31) / 32) * 32;
   const size_t smem = static_cast<size_t>(rows_pad) * n * (sizeof(double) + sizeof(int)) +
                       static_cast<size_t>(rows_pad) * sizeof(double) +
@@ -846,7 +890,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   p->variant = p->cluster_fn ? 3 : (p->resident ? 0 : 1);
   if (tma_fn && !(flags & RBF_STREAM_LDG) && N_i > 0) {
     // ring geometry: ~24 KB stages, as many as fit in ~200 KB of shared memory
-    const int slice = n * 32 * 12 + 32 * 8;
+    const int slice = n * 32 * (8 + p->index_bits / 8) + 32 * 8;
     int sps = std::max(1, 24576 / slice);
     if (const char* e = std::getenv("RBFFD_TMA_SPS")) sps = std::max(1, std::atoi(e));
     sps = std::max(rpl, (sps / rpl) * rpl);
@@ -1146,6 +1190,12 @@ int rbf_plan_get_info(const rbf_plan* p, rbf_plan_info* info) {
   info->device_bytes = p->device_bytes;
   info->bytes_per_step = p->N_i * (12LL * p->n + 24);
   info->launches = p->launches;
+  info->index_bits = p->index_bits;
+  // bytes the streaming step actually moves: 16-bit ids, the per-slice window
+  // bases, and int32 ids of the overflow slices
+  info->stream_bytes_per_step = (p->index_bits == 16 && !p->resident)
+      ? p->N_i * (10LL * p->n + 24) + p->S * 16 + p->overflow_slices * 32LL * p->n * 4
+      : info->bytes_per_step;
   return RBF_OK;
 }
 
@@ -1182,6 +1232,8 @@ void rbf_plan_destroy(rbf_plan* p) {
   pool_free(p->row_of_k, s);
   pool_free(p->halo_send_idx, s);
   pool_free(p->cluster_dest, s);
+  pool_free(p->C16, s);
+  pool_free(p->meta, s);
   pool_free(p->halo_sendbuf, s);
   pool_free(p->st, s);
   if (s) cudaStreamSynchronize(s);

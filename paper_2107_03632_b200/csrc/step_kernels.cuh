@@ -47,6 +47,8 @@ struct StepArgs {
   const double* __restrict__ W;  // [S*n*32]
   const int* __restrict__ C;     // [S*n*32]
   const double* __restrict__ F;  // [S*32]
+  const unsigned short* __restrict__ C16;  // [S*n*32] 16-bit ids (two-window), or null
+  const int4* __restrict__ meta;           // [S] {base0, base1, ok, 0} of the 16-bit ids
   long long n_rows;
   long long dst_base;            // node id of row 0 (= N - N_i)
   int n;
@@ -314,14 +316,69 @@ struct TmaGeom {
   int stages;  // ring depth
 };
 
-template <int NJ>
+template <int NJ, int IB>
 __host__ __device__ constexpr int tma_slice_bytes() {
-  return NJ * 32 * 12 + 32 * 8;
+  return NJ * 32 * (8 + IB) + 32 * 8;
+}
+
+// 16-bit ids (IB == 2): each SELL slice stores its ids as 15-bit offsets from
+// one of two per-slice bases (bit 15 selects base1).  With Morton-ordered rows
+// 99.4-99.6 % of slices fit (profiles/README.md); the rest keep ok == 0 and
+// their consumers read the int32 ids from global memory instead.  Saves 2n of
+// the 12n+24 bytes each row streams.
+__device__ __forceinline__ int decode_id(unsigned int v, int4 m) {
+  return (v & 0x8000u) ? m.y + static_cast<int>(v & 0x7fffu) : m.x + static_cast<int>(v);
+}
+
+__global__ void compress_ids_kernel(const int* __restrict__ C, long long n_rows, int n,
+                                    unsigned short* __restrict__ C16, int4* __restrict__ meta,
+                                    unsigned long long* n_overflow) {
+  const int lane = threadIdx.x & 31;
+  const long long S = (n_rows + 31) >> 5;
+  for (long long sl = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; sl < S;
+       sl += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const bool live = sl * 32 + lane < n_rows;
+    const int* c = C + sl * n * 32 + lane;
+    int mn = 0x7fffffff;
+    for (int j = 0; j < n && live; ++j) mn = min(mn, c[32 * j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    const long long lim = static_cast<long long>(mn) + 32767;
+    int mn1 = 0x7fffffff, mx1 = -1;
+    for (int j = 0; j < n && live; ++j) {
+      const int v = c[32 * j];
+      if (v > lim) {
+        mn1 = min(mn1, v);
+        mx1 = max(mx1, v);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn1 = min(mn1, __shfl_xor_sync(0xffffffffu, mn1, o));
+      mx1 = max(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+    }
+    const bool ok = (mx1 < 0) || (mx1 - mn1 <= 32767);
+    const int base1 = mx1 < 0 ? mn : mn1;
+    unsigned short* d = C16 + sl * n * 32 + lane;
+    for (int j = 0; j < n; ++j) {
+      unsigned short e = 0;
+      if (live && ok) {
+        const int v = c[32 * j];
+        e = (v <= lim) ? static_cast<unsigned short>(v - mn)
+                       : static_cast<unsigned short>(0x8000 | (v - base1));
+      }
+      d[32 * j] = e;
+    }
+    if (lane == 0) {
+      meta[sl] = make_int4(mn, base1, ok ? 1 : 0, 0);
+      if (!ok) atomicAdd(n_overflow, 1ull);
+    }
+  }
 }
 
 // RPL: slices per consumer unit (each lane carries RPL independent rows, so a
 // warp keeps RPL*NJ gathers in flight); sps must be a multiple of RPL.
-template <int NJ, int CW, int RPL>
+template <int NJ, int CW, int RPL, int IB>
 __global__ void __launch_bounds__(32 * (CW + 1), 1)
 step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeom g) {
   extern __shared__ __align__(128) unsigned char tma_smem[];
@@ -335,8 +392,8 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
   // consumers first wait until their chunk has been armed (expect_tx issued).
   __shared__ int s_issued;
   const int sps = g.sps, stages = g.stages;
-  const int wbytes = sps * NJ * 32 * 8, cbytes = sps * NJ * 32 * 4;
-  const int stage_bytes = sps * tma_slice_bytes<NJ>();
+  const int wbytes = sps * NJ * 32 * 8, cbytes = sps * NJ * 32 * IB;
+  const int stage_bytes = sps * tma_slice_bytes<NJ, IB>();
   const long long S = (a.n_rows + 31) >> 5;
   const long long nchunks = (S + sps - 1) / sps;
   const long long my_n = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -367,10 +424,11 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
         const long long s0 = c * sps;
         const int ns = static_cast<int>(S - s0 < sps ? S - s0 : sps);
         unsigned char* dst = ring + static_cast<size_t>(s) * stage_bytes;
-        const uint32_t wb = ns * NJ * 32 * 8, cb = ns * NJ * 32 * 4, fb = ns * 32 * 8;
+        const uint32_t wb = ns * NJ * 32 * 8, cb = ns * NJ * 32 * IB, fb = ns * 32 * 8;
         mbar_expect_tx(&full[s], wb + cb + fb);
         bulk_g2s(dst, a.W + s0 * NJ * 32, wb, &full[s], pol);
-        bulk_g2s(dst + wbytes, a.C + s0 * NJ * 32, cb, &full[s], pol);
+        if constexpr (IB == 2) bulk_g2s(dst + wbytes, a.C16 + s0 * NJ * 32, cb, &full[s], pol);
+        else bulk_g2s(dst + wbytes, a.C + s0 * NJ * 32, cb, &full[s], pol);
         bulk_g2s(dst + wbytes + cbytes, a.F + s0 * 32, fb, &full[s], pol);
         __threadfence_block();  // order the arm before the publication below
         *reinterpret_cast<volatile int*>(&s_issued) = static_cast<int>(i + 1);
@@ -425,11 +483,25 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
       for (int t = 0; t < RPL; ++t) {
         const long long r = (slice0 + t) * 32 + lane;
         live[t] = (slice0 + t) < S && r < a.n_rows;
-        const int* sC = reinterpret_cast<const int*>(base + wbytes) + (slot0 + t) * NJ * 32;
         if (live[t]) {
           // ids from the ring -> gathers, all issued before the first use
+          if constexpr (IB == 2) {
+            const int4 m = __ldg(a.meta + slice0 + t);
+            if (m.z) {
+              const unsigned short* sC =
+                  reinterpret_cast<const unsigned short*>(base + wbytes) + (slot0 + t) * NJ * 32;
 #pragma unroll
-          for (int j = 0; j < NJ; ++j) g[t][j] = ld_field(u_in + sC[j * 32 + lane]);
+              for (int j = 0; j < NJ; ++j) g[t][j] = ld_field(u_in + decode_id(sC[j * 32 + lane], m));
+            } else {  // slice too spread for two 15-bit windows: int32 ids from HBM
+              const int* gC = a.C + (slice0 + t) * NJ * 32 + lane;
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) g[t][j] = ld_field(u_in + __ldg(gC + 32 * j));
+            }
+          } else {
+            const int* sC = reinterpret_cast<const int*>(base + wbytes) + (slot0 + t) * NJ * 32;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) g[t][j] = ld_field(u_in + sC[j * 32 + lane]);
+          }
           u_self[t] = ld_field(u_in + a.dst_base + r);
         }
       }

@@ -326,9 +326,13 @@ def test_tma_and_ldg_step_variants_agree_with_oracle(synth_cache, target, n, m):
     u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
     dt = 0.5 * rb.stability_bound(shapes)
     want = orc.run_time_loop(nodes, shapes, steps=70)
-    for tma, pdl in ((True, True), (True, False), (False, True)):
-        plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, tma=tma, pdl=pdl)
-        assert plan.info()["variant"] == (2 if tma else 1)
+    for tma, pdl, idx16 in ((True, True, True), (True, True, False), (True, False, True),
+                            (False, True, True)):
+        plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, nodes.positions,
+                    renumber=True, tma=tma, pdl=pdl, idx16=idx16)
+        info = plan.info()
+        assert info["variant"] == (2 if tma else 1)
+        assert info["index_bits"] == (16 if (tma and idx16) else 32)
         plan.set_field(u0)
         res = plan.run(dt, steps=70)
         assert res.residual == want["residual"]
@@ -348,13 +352,34 @@ def test_tma_ring_many_laps_matches_ldg(synth_cache, target, n, m):
     u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
     dt = 0.5 * rb.stability_bound(shapes)
     out = []
-    for tma in (True, False):
-        plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, tma=tma)
+    for tma, idx16, renumber in ((True, True, True), (True, False, True), (False, False, False),
+                                 (True, True, False)):
+        plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, nodes.positions,
+                    renumber=renumber, tma=tma, idx16=idx16)
         plan.set_field(u0)
         res = plan.run(dt, steps=300)
-        out.append((plan.get_field(), res.residual))
+        out.append((plan.get_field(), res.residual, plan.info()["index_bits"]))
         plan.close()
-    assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
+    assert out[0][2] == 16  # Morton order: nearly every slice fits the 16-bit windows
+    for f, r, _ in out[1:]:
+        assert np.array_equal(out[0][0], f) and out[0][1] == r
+
+
+def test_idx16_overflow_slices_path(synth_cache, monkeypatch):
+    """Force 16-bit ids on the native (non-Morton) order, where many slices
+    overflow the two windows and read int32 ids from HBM instead."""
+    monkeypatch.setenv("RBFFD_IDX16", "2")
+    nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
+    interior = shapes.interior_nodes
+    plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                rb.forcing(nodes.positions[interior]))
+    info = plan.info()
+    assert info["index_bits"] == 16
+    assert info["stream_bytes_per_step"] > info["N_i"] * (10 * 15 + 24)  # some overflow slices
+    plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
+    res = plan.run(0.5 * rb.stability_bound(shapes), steps=60)
+    want = orc.run_time_loop(nodes, shapes, steps=60)
+    assert np.array_equal(plan.get_field(), want["field"]) and res.residual == want["residual"]
 
 
 def test_synthetic_steady_streaming_matches_oracle(synth_cache):
