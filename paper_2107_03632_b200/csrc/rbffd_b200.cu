@@ -890,7 +890,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   p->variant = p->cluster_fn ? 3 : (p->resident ? 0 : 1);
   if (tma_fn && !(flags & RBF_STREAM_LDG) && N_i > 0) {
     // ring geometry: ~24 KB stages, as many as fit in ~200 KB of shared memory
-    const int slice = n * 32 * (8 + p->index_bits / 8) + 32 * 8;
+    const int slice = n * 32 * (8 + p->index_bits / 8) + 32 * 8 + (p->index_bits == 16 ? 16 : 0);
     int sps = std::max(1, 24576 / slice);
     if (const char* e = std::getenv("RBFFD_TMA_SPS")) sps = std::max(1, std::atoi(e));
     sps = std::max(rpl, (sps / rpl) * rpl);

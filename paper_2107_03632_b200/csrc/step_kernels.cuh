@@ -318,7 +318,7 @@ struct TmaGeom {
 
 template <int NJ, int IB>
 __host__ __device__ constexpr int tma_slice_bytes() {
-  return NJ * 32 * (8 + IB) + 32 * 8;
+  return NJ * 32 * (8 + IB) + 32 * 8 + (IB == 2 ? 16 : 0);  // + the slice's window bases
 }
 
 // 16-bit ids (IB == 2): each SELL slice stores its ids as 15-bit offsets from
@@ -425,10 +425,15 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
         const int ns = static_cast<int>(S - s0 < sps ? S - s0 : sps);
         unsigned char* dst = ring + static_cast<size_t>(s) * stage_bytes;
         const uint32_t wb = ns * NJ * 32 * 8, cb = ns * NJ * 32 * IB, fb = ns * 32 * 8;
-        mbar_expect_tx(&full[s], wb + cb + fb);
+        const uint32_t mb = IB == 2 ? ns * 16 : 0;
+        mbar_expect_tx(&full[s], wb + cb + fb + mb);
         bulk_g2s(dst, a.W + s0 * NJ * 32, wb, &full[s], pol);
-        if constexpr (IB == 2) bulk_g2s(dst + wbytes, a.C16 + s0 * NJ * 32, cb, &full[s], pol);
-        else bulk_g2s(dst + wbytes, a.C + s0 * NJ * 32, cb, &full[s], pol);
+        if constexpr (IB == 2) {
+          bulk_g2s(dst + wbytes, a.C16 + s0 * NJ * 32, cb, &full[s], pol);
+          bulk_g2s(dst + wbytes + cbytes + sps * 32 * 8, a.meta + s0, mb, &full[s], pol);
+        } else {
+          bulk_g2s(dst + wbytes, a.C + s0 * NJ * 32, cb, &full[s], pol);
+        }
         bulk_g2s(dst + wbytes + cbytes, a.F + s0 * 32, fb, &full[s], pol);
         __threadfence_block();  // order the arm before the publication below
         *reinterpret_cast<volatile int*>(&s_issued) = static_cast<int>(i + 1);
@@ -485,24 +490,33 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
         live[t] = (slice0 + t) < S && r < a.n_rows;
         if (live[t]) {
           // ids from the ring -> gathers, all issued before the first use
+          int c0;
           if constexpr (IB == 2) {
-            const int4 m = __ldg(a.meta + slice0 + t);
+            const int4 m = reinterpret_cast<const int4*>(base + wbytes + cbytes + sps * 32 * 8)[slot0 + t];
             if (m.z) {
               const unsigned short* sC =
                   reinterpret_cast<const unsigned short*>(base + wbytes) + (slot0 + t) * NJ * 32;
+              c0 = decode_id(sC[lane], m);
+              g[t][0] = ld_field(u_in + c0);
 #pragma unroll
-              for (int j = 0; j < NJ; ++j) g[t][j] = ld_field(u_in + decode_id(sC[j * 32 + lane], m));
+              for (int j = 1; j < NJ; ++j) g[t][j] = ld_field(u_in + decode_id(sC[j * 32 + lane], m));
             } else {  // slice too spread for two 15-bit windows: int32 ids from HBM
               const int* gC = a.C + (slice0 + t) * NJ * 32 + lane;
+              c0 = __ldg(gC);
+              g[t][0] = ld_field(u_in + c0);
 #pragma unroll
-              for (int j = 0; j < NJ; ++j) g[t][j] = ld_field(u_in + __ldg(gC + 32 * j));
+              for (int j = 1; j < NJ; ++j) g[t][j] = ld_field(u_in + __ldg(gC + 32 * j));
             }
           } else {
             const int* sC = reinterpret_cast<const int*>(base + wbytes) + (slot0 + t) * NJ * 32;
+            c0 = sC[lane];
+            g[t][0] = ld_field(u_in + c0);
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) g[t][j] = ld_field(u_in + sC[j * 32 + lane]);
+            for (int j = 1; j < NJ; ++j) g[t][j] = ld_field(u_in + sC[j * 32 + lane]);
           }
-          u_self[t] = ld_field(u_in + a.dst_base + r);
+          // stencils list the centre first (neighborhoods.py:29-32): reuse it
+          const long long node = a.dst_base + r;
+          u_self[t] = (c0 == node) ? g[t][0] : ld_field(u_in + node);
         }
       }
 #pragma unroll
