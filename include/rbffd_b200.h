@@ -53,6 +53,7 @@ extern "C" {
 #define RBF_STREAM_LDG 0x8u       /* streaming step with plain loads instead of the TMA ring */
 #define RBF_NO_CLUSTER 0x10u      /* small problems: single-CTA resident loop, not the cluster loop */
 #define RBF_NO_IDX16 0x20u        /* keep int32 node ids in the streamed step (no 16-bit windows) */
+#define RBF_NO_FLOW 0x40u         /* fixed-step runs: graph of step launches, not the persistent dataflow loop */
 
 /* run modes (SolveConfig.mode, solver.py:53) */
 #define RBF_MODE_FIXED 0
@@ -162,8 +163,11 @@ typedef struct rbf_plan_info {
   int32_t kernel_n;        /* compile-time width of the chosen step kernel (0: generic) */
   int32_t grid, block;     /* streaming kernel launch geometry */
   int32_t variant;         /* 0 resident loop (1 CTA), 1 LDG streaming step, 2 TMA-ring
-                              streaming step, 3 cluster-resident loop (DSMEM halo) */
+                              streaming step, 3 cluster-resident loop (DSMEM halo); fixed-step
+                              runs of variant 2 use the persistent dataflow loop when flow == 1 */
   int32_t index_bits;      /* 32, or 16: two-window 16-bit ids streamed by the TMA step */
+  int32_t flow;            /* 1: fixed-step runs use the persistent dataflow loop */
+  int32_t flow_grid;       /* its CTAs (one per SM) */
   int64_t device_bytes;    /* device memory held by the plan */
   int64_t bytes_per_step;  /* algorithmic HBM bytes per step: N_i*(12n+24) */
   int64_t launches;        /* kernel launches issued by this plan so far */

@@ -17,6 +17,7 @@
 #include "../../include/rbffd_b200.h"
 #include "step_kernels.cuh"
 #include "weights_kernels.cuh"
+#include "flow_kernels.cuh"
 
 #include <cuda_runtime.h>
 
@@ -64,6 +65,7 @@ using StreamFn = void (*)(rbf::StepArgs, const double*, double*, int);
 using TmaFn = void (*)(rbf::StepArgs, const double*, double*, int, rbf::TmaGeom);
 using ResidentFn = void (*)(rbf::ResidentArgs);
 using ClusterFn = void (*)(rbf::ClusterArgs);
+using FlowFn = void (*)(rbf::FlowArgs, rbf::TmaGeom);
 
 template <int NJ>
 struct KernelSet {
@@ -87,6 +89,14 @@ struct KernelSet {
     }
   }
   static int rpl(int rpl_req) { return (rpl_req == 2 && NJ > 0 && NJ <= 20) ? 2 : 1; }
+  static FlowFn flow(bool idx16) {
+    if constexpr (NJ > 0) {
+      return idx16 ? rbf::step_flow_kernel<NJ, kCW, 2> : rbf::step_flow_kernel<NJ, kCW, 4>;
+    } else {
+      (void)idx16;
+      return nullptr;
+    }
+  }
   static int cw() { return kCW; }
 };
 
@@ -194,6 +204,13 @@ struct rbf_plan {
   int4* meta = nullptr;            // per-slice {base0, base1, ok, 0}
   int index_bits = 32;
   int64_t overflow_slices = 0;
+  // persistent dataflow loop for fixed-step runs (flow_kernels.cuh)
+  FlowFn flow_fn = nullptr;
+  int flow_grid = 0, flow_spc = 0;
+  int* flow_flags = nullptr;
+  int* flow_dep_off = nullptr;
+  int* flow_dep = nullptr;
+  double* u_init = nullptr;        // start field kept for the exact re-run after a failure
   int kernel_n = 0;
   bool resident = false;
   size_t resident_smem = 0;
@@ -456,6 +473,53 @@ int run_streaming(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
   cudaEventDestroy(evs[0]);
   cudaEventDestroy(evs[1]);
   return rc;
+}
+
+// Fixed-step loop in one persistent launch (flow_kernels.cuh).  Returns
+// RBF_OK with *fallback = true when a non-finite value appeared: the caller
+// then replays the run on the graph path, which stops at the exact step.
+int run_flow(rbf_plan* p, int64_t limit, bool* fallback) {
+  *fallback = false;
+  p->h_st->bad_step = std::numeric_limits<long long>::max();
+  RBF_CK(cudaMemcpyAsync(p->st, p->h_st, sizeof(rbf::DevStatus), cudaMemcpyHostToDevice, p->stream));
+  RBF_CK(cudaMemcpyAsync(p->u_init, p->U[0], sizeof(double) * p->N, cudaMemcpyDeviceToDevice, p->stream));
+  RBF_CK(cudaMemsetAsync(p->flow_flags, 0, sizeof(int) * p->flow_grid, p->stream));
+  rbf::FlowArgs fa;
+  fa.a = p->args();
+  fa.U0 = p->U[0];
+  fa.U1 = p->U[1];
+  fa.flags = p->flow_flags;
+  fa.dep_off = p->flow_dep_off;
+  fa.dep = p->flow_dep;
+  fa.steps = limit;
+  fa.spc = p->flow_spc;
+  fa.need_res_last = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p->flow_grid);
+  cfg.blockDim = dim3(p->tma_block);
+  cfg.dynamicSmemBytes = p->tma_smem;
+  cfg.stream = p->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: neighbour waits are safe
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RBF_CK(cudaEventRecord(p->ev0, p->stream));
+  RBF_CK(cudaLaunchKernelEx(&cfg, p->flow_fn, fa, p->tma_geom));
+  rbf::flow_finalize_kernel<<<1, 32, 0, p->stream>>>(p->st, limit, 1);
+  RBF_CK(cudaGetLastError());
+  RBF_CK(cudaEventRecord(p->ev1, p->stream));
+  p->launches += 2;
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  rbf::DevStatus s;
+  RBF_CK(cudaMemcpy(&s, p->st, sizeof(s), cudaMemcpyDeviceToHost));
+  if (s.bad_step >= 0) {
+    // restore the start field (both buffers) and let the caller replay exactly
+    RBF_CK(cudaMemcpyAsync(p->U[0], p->u_init, sizeof(double) * p->N, cudaMemcpyDeviceToDevice, p->stream));
+    RBF_CK(cudaMemcpyAsync(p->U[1], p->u_init, sizeof(double) * p->N, cudaMemcpyDeviceToDevice, p->stream));
+    *fallback = true;
+  }
+  return RBF_OK;
 }
 
 int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
@@ -912,6 +976,66 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
       cudaGetLastError();
     }
   }
+  // dataflow loop: one CTA per SM, contiguous slice ranges, neighbour waits
+  if (p->tma_fn && !(flags & RBF_NO_FLOW) && !(std::getenv("RBFFD_FLOW") && std::atoi(std::getenv("RBFFD_FLOW")) == 0)) {
+    FlowFn ffn = nullptr;
+    switch (n) {
+#define RBF_FCASE(K) \
+  case K:            \
+    ffn = KernelSet<K>::flow(p->index_bits == 16); \
+    break;
+      RBF_SPECIALISED(RBF_FCASE)
+#undef RBF_FCASE
+      default:
+        ffn = nullptr;
+    }
+    int occ = 0;
+    if (ffn && set_max_smem(ffn) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ffn, p->tma_block, p->tma_smem) == cudaSuccess &&
+        occ >= 1) {
+      const int G = sms;  // one CTA per SM (the ring fills the shared memory)
+      const int spc = static_cast<int>((p->S + G - 1) / G);
+      if (p->S >= 4LL * G && spc >= p->tma_geom.sps) {
+        const int words = (G + 31) / 32;
+        unsigned int* d_mat = nullptr;
+        RBF_TRY(pool_alloc(&d_mat, static_cast<size_t>(G) * words, p->stream));
+        RBF_CK(cudaMemsetAsync(d_mat, 0, sizeof(unsigned int) * G * words, p->stream));
+        const int blocks = static_cast<int>(std::min<int64_t>((N_i * n + 255) / 256, 148 * 16));
+        rbf::flow_dep_kernel<<<blocks, 256, 0, p->stream>>>(p->C, N_i, n, B, static_cast<long long>(spc) * 32,
+                                                            words, d_mat);
+        RBF_CK(cudaGetLastError());
+        std::vector<unsigned int> mat(static_cast<size_t>(G) * words);
+        RBF_CK(cudaMemcpyAsync(mat.data(), d_mat, sizeof(unsigned int) * mat.size(), cudaMemcpyDeviceToHost,
+                               p->stream));
+        RBF_CK(cudaStreamSynchronize(p->stream));
+        pool_free(d_mat, p->stream);
+        std::vector<int> off(G + 1, 0), dep;
+        int maxdeg = 0;
+        for (int b = 0; b < G; ++b) {
+          for (int c = 0; c < G; ++c)
+            if (mat[static_cast<size_t>(b) * words + (c >> 5)] & (1u << (c & 31))) dep.push_back(c);
+          off[b + 1] = static_cast<int>(dep.size());
+          maxdeg = std::max(maxdeg, off[b + 1] - off[b]);
+        }
+        if (maxdeg <= 160) {
+          RBF_TRY(dev_alloc(p.get(), &p->flow_dep_off, static_cast<size_t>(G + 1)));
+          RBF_TRY(dev_alloc(p.get(), &p->flow_dep, std::max<size_t>(1, dep.size())));
+          RBF_TRY(dev_alloc(p.get(), &p->flow_flags, static_cast<size_t>(G)));
+          RBF_TRY(dev_alloc(p.get(), &p->u_init, static_cast<size_t>(N)));
+          RBF_CK(cudaMemcpyAsync(p->flow_dep_off, off.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice,
+                                 p->stream));
+          if (!dep.empty())
+            RBF_CK(cudaMemcpyAsync(p->flow_dep, dep.data(), sizeof(int) * dep.size(), cudaMemcpyHostToDevice,
+                                   p->stream));
+          RBF_CK(cudaStreamSynchronize(p->stream));
+          p->flow_fn = ffn;
+          p->flow_grid = G;
+          p->flow_spc = spc;
+        }
+      }
+    }
+    cudaGetLastError();
+  }
   if (!p->tma_fn) {
     RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p->stream_fn, kStreamBlock, 0));
     per_sm = std::max(per_sm, 1);
@@ -1089,8 +1213,18 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
   RBF_TRY(reset_status(p, dt, tol));
   int rc;
   PhaseTimer timer;
-  if (p->resident) rc = run_resident(p, limit, steady, copy_back != 0);
-  else rc = run_streaming(p, limit, steady, copy_back != 0);
+  if (p->resident) {
+    rc = run_resident(p, limit, steady, copy_back != 0);
+  } else if (p->flow_fn && !steady && !copy_back && limit >= 2) {
+    bool fallback = false;
+    rc = run_flow(p, limit, &fallback);
+    if (rc == RBF_OK && fallback) {
+      RBF_TRY(reset_status(p, dt, tol));
+      rc = run_streaming(p, limit, steady, false);
+    }
+  } else {
+    rc = run_streaming(p, limit, steady, copy_back != 0);
+  }
   if (rc != RBF_OK) return rc;
   RBF_CK(cudaStreamSynchronize(p->stream));
   timer.mark("run total (incl. sync)");
@@ -1191,6 +1325,8 @@ int rbf_plan_get_info(const rbf_plan* p, rbf_plan_info* info) {
   info->bytes_per_step = p->N_i * (12LL * p->n + 24);
   info->launches = p->launches;
   info->index_bits = p->index_bits;
+  info->flow = p->flow_fn ? 1 : 0;
+  info->flow_grid = p->flow_grid;
   // bytes the streaming step actually moves: 16-bit ids, the per-slice window
   // bases, and int32 ids of the overflow slices
   info->stream_bytes_per_step = (p->index_bits == 16 && !p->resident)
@@ -1234,6 +1370,10 @@ void rbf_plan_destroy(rbf_plan* p) {
   pool_free(p->cluster_dest, s);
   pool_free(p->C16, s);
   pool_free(p->meta, s);
+  pool_free(p->flow_flags, s);
+  pool_free(p->flow_dep_off, s);
+  pool_free(p->flow_dep, s);
+  pool_free(p->u_init, s);
   pool_free(p->halo_sendbuf, s);
   pool_free(p->st, s);
   if (s) cudaStreamSynchronize(s);

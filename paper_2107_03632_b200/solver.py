@@ -154,7 +154,8 @@ class Plan:
 
     def __init__(self, n_total, interior, rows, weights, f_int, positions=None, *,
                  renumber: bool = False, device: int = 0, resident: bool = True,
-                 pdl: bool = True, tma: bool = True, cluster: bool = True, idx16: bool = True):
+                 pdl: bool = True, tma: bool = True, cluster: bool = True, idx16: bool = True,
+                 flow: bool = True):
         self._lib = _lib.load()
         interior = _as(interior, np.int64)
         weights = _as(weights, np.float64)
@@ -182,6 +183,8 @@ class Plan:
             flags |= _lib.RBF_NO_CLUSTER
         if not idx16:
             flags |= _lib.RBF_NO_IDX16
+        if not flow:
+            flags |= _lib.RBF_NO_FLOW
         handle = ctypes.c_void_p()
         rc = self._lib.rbf_plan_create(
             ctypes.byref(handle), int(n_total), int(n_rows), int(n), _ptr(interior), _ptr(rows),

@@ -326,13 +326,15 @@ def test_tma_and_ldg_step_variants_agree_with_oracle(synth_cache, target, n, m):
     u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
     dt = 0.5 * rb.stability_bound(shapes)
     want = orc.run_time_loop(nodes, shapes, steps=70)
-    for tma, pdl, idx16 in ((True, True, True), (True, True, False), (True, False, True),
-                            (False, True, True)):
+    for tma, pdl, idx16, flow in ((True, True, True, True), (True, True, False, True),
+                                  (True, True, True, False), (True, False, True, False),
+                                  (True, True, False, False), (False, True, True, True)):
         plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, nodes.positions,
-                    renumber=True, tma=tma, pdl=pdl, idx16=idx16)
+                    renumber=True, tma=tma, pdl=pdl, idx16=idx16, flow=flow)
         info = plan.info()
         assert info["variant"] == (2 if tma else 1)
         assert info["index_bits"] == (16 if (tma and idx16) else 32)
+        assert info["flow"] == (1 if (tma and flow) else 0)
         plan.set_field(u0)
         res = plan.run(dt, steps=70)
         assert res.residual == want["residual"]
@@ -363,6 +365,40 @@ def test_tma_ring_many_laps_matches_ldg(synth_cache, target, n, m):
     assert out[0][2] == 16  # Morton order: nearly every slice fits the 16-bit windows
     for f, r, _ in out[1:]:
         assert np.array_equal(out[0][0], f) and out[0][1] == r
+
+
+def test_flow_loop_failure_replays_the_exact_step(synth_cache):
+    """The persistent dataflow loop only records that a non-finite value
+    appeared; the run is replayed on the graph path so the failing step and
+    the failing field are the reference's (solver.py:200-206)."""
+    nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
+    interior = shapes.interior_nodes
+    plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                rb.forcing(nodes.positions[interior]))
+    assert plan.info()["flow"] == 1
+    dt = 40.0 * rb.stability_bound(shapes)
+    want = orc.run_time_loop(nodes, shapes, dt=dt, steps=200)
+    assert want["status"] == orc.ORC_INSTABILITY
+    plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
+    res = plan.run(dt, steps=200)
+    assert res.status == _lib.RBF_ERR_INSTABILITY and res.bad_step == want["step"]
+    got = plan.get_field()
+    assert np.array_equal(got, want["field"], equal_nan=True)
+    # and the plan keeps working after the replay
+    plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
+    res = plan.run(0.5 * rb.stability_bound(shapes), steps=77)
+    want = orc.run_time_loop(nodes, shapes, steps=77)
+    assert np.array_equal(plan.get_field(), want["field"]) and res.residual == want["residual"]
+
+
+@pytest.mark.parametrize("steps", [2, 3, 64, 65, 129])
+def test_flow_loop_step_counts(synth_cache, steps):
+    nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
+    want = orc.run_time_loop(nodes, shapes, steps=steps)
+    cfg = rb.SolveConfig(degree=2, support_size=15, nodes=200_000, steps=steps)
+    rep = rb.run_time_loop(cfg, nodes, shapes)
+    assert np.array_equal(rep.field, want["field"]) and rep.residual == want["residual"]
+    assert rep.steps == steps
 
 
 def test_idx16_overflow_slices_path(synth_cache, monkeypatch):
