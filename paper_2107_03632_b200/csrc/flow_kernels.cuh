@@ -192,14 +192,19 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) step_flow_kernel(FlowArgs fa
     if (last) break;
     // ---- step edge: publish step, wait for the neighbour CTAs ------------
     consumer_bar(ncons);  // every consumer of this CTA finished the step
-    if (threadIdx.x == 32) {
-      __threadfence();
-      st_release_gpu(fa.flags + b, static_cast<int>(step + 1));
-      for (int k = 0; k < s_ndep; ++k) {
-        const int* f = fa.flags + s_dep[k];
-        while (ld_acquire_gpu(f) < step + 1) __nanosleep(32);
+    if (warp == 1) {
+      if (lane == 0) {
+        __threadfence();
+        st_release_gpu(fa.flags + b, static_cast<int>(step + 1));
       }
-      __threadfence();  // gpu-scope fence: invalidates this SM's L1 before the next gathers
+      // poll the neighbours in parallel (relaxed), then one acquire fence
+      for (int k = lane; k < s_ndep; k += 32) {
+        const volatile int* f = fa.flags + s_dep[k];
+        while (*f < step + 1) __nanosleep(20);
+      }
+      __syncwarp();
+      if (lane == 0) __threadfence();  // gpu-scope fence: acquire, and invalidates this SM's L1
+      __syncwarp();
     }
     consumer_bar(ncons);
   }
