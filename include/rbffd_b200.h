@@ -53,7 +53,8 @@ extern "C" {
 #define RBF_STREAM_LDG 0x8u       /* streaming step with plain loads instead of the TMA ring */
 #define RBF_NO_CLUSTER 0x10u      /* small problems: single-CTA resident loop, not the cluster loop */
 #define RBF_NO_IDX16 0x20u        /* keep int32 node ids in the streamed step (no 16-bit windows) */
-#define RBF_NO_FLOW 0x40u         /* fixed-step runs: graph of step launches, not the persistent dataflow loop */
+#define RBF_FLOW 0x40u            /* opt-in: fixed-step runs in the persistent dataflow loop (measured
+                                     slower than the graph path on B200, profiles/README.md) */
 
 /* run modes (SolveConfig.mode, solver.py:53) */
 #define RBF_MODE_FIXED 0

@@ -26,7 +26,7 @@ RBF_NO_PDL = 0x4
 RBF_STREAM_LDG = 0x8
 RBF_NO_CLUSTER = 0x10
 RBF_NO_IDX16 = 0x20
-RBF_NO_FLOW = 0x40
+RBF_FLOW = 0x40
 
 RBF_MODE_FIXED = 0
 RBF_MODE_STEADY = 1

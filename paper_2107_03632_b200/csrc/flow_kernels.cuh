@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) step_flow_kernel(FlowArgs fa
     consumer_bar(ncons);  // every consumer of this CTA finished the step
     if (warp == 1) {
       if (lane == 0) {
-        __threadfence();
+        // bar.sync ordered every consumer's stores before this release (cumulative)
         st_release_gpu(fa.flags + b, static_cast<int>(step + 1));
       }
       // poll the neighbours in parallel (relaxed), then one acquire fence

@@ -964,7 +964,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
     const size_t smem_t = 2 * 16 * sizeof(uint64_t) + static_cast<size_t>(stages) * stage;
     if (smem_t <= kResidentSmemMax && set_max_smem(tma_fn) == cudaSuccess) {
       p->tma_fn = tma_fn;
-      p->tma_geom = rbf::TmaGeom{sps, stages};
+      p->tma_geom = rbf::TmaGeom{sps, stages, std::getenv("RBFFD_TMA_CONTIG") ? 1 : 0};
       p->tma_smem = smem_t;
       p->tma_block = 32 * (cw + 1);
       const int64_t chunks = (p->S + sps - 1) / sps;
@@ -977,7 +977,8 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
     }
   }
   // dataflow loop: one CTA per SM, contiguous slice ranges, neighbour waits
-  if (p->tma_fn && !(flags & RBF_NO_FLOW) && !(std::getenv("RBFFD_FLOW") && std::atoi(std::getenv("RBFFD_FLOW")) == 0)) {
+  const char* flow_env = std::getenv("RBFFD_FLOW");
+  if (p->tma_fn && ((flags & RBF_FLOW) || (flow_env && std::atoi(flow_env) == 1))) {
     FlowFn ffn = nullptr;
     switch (n) {
 #define RBF_FCASE(K) \

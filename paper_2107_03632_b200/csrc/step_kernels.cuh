@@ -317,6 +317,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 struct TmaGeom {
   int sps;     // slices per chunk (stage)
   int stages;  // ring depth
+  int contig;  // experiment: CTA b takes a contiguous range of chunks instead of b, b+G, ...
 };
 
 template <int NJ, int IB>
@@ -399,7 +400,10 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
   const int stage_bytes = sps * tma_slice_bytes<NJ, IB>();
   const long long S = (a.n_rows + 31) >> 5;
   const long long nchunks = (S + sps - 1) / sps;
-  const long long my_n = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long cpc = (nchunks + gridDim.x - 1) / gridDim.x;
+  const long long my_n = g.contig
+      ? (blockIdx.x * cpc < nchunks ? (nchunks - blockIdx.x * cpc < cpc ? nchunks - blockIdx.x * cpc : cpc) : 0)
+      : (blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -423,7 +427,8 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
       const uint64_t pol = policy_evict_first();
       auto issue = [&](long long i) {
         const int s = static_cast<int>(i % stages);
-        const long long c = blockIdx.x + i * gridDim.x;
+        const long long c = g.contig ? blockIdx.x * ((nchunks + gridDim.x - 1) / gridDim.x) + i
+                                     : blockIdx.x + i * gridDim.x;
         const long long s0 = c * sps;
         const int ns = static_cast<int>(S - s0 < sps ? S - s0 : sps);
         unsigned char* dst = ring + static_cast<size_t>(s) * stage_bytes;
@@ -483,7 +488,7 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
       __syncwarp();
       mbar_wait(&full[s], static_cast<uint32_t>((i / stages) & 1));
       const unsigned char* base = ring + static_cast<size_t>(s) * stage_bytes;
-      const long long slice0 = (blockIdx.x + i * gridDim.x) * sps + slot0;
+      const long long slice0 = (g.contig ? blockIdx.x * cpc + i : blockIdx.x + i * gridDim.x) * sps + slot0;
       bool live[RPL];
       double g[RPL][NJ];
       double u_self[RPL];

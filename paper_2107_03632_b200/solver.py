@@ -155,7 +155,7 @@ class Plan:
     def __init__(self, n_total, interior, rows, weights, f_int, positions=None, *,
                  renumber: bool = False, device: int = 0, resident: bool = True,
                  pdl: bool = True, tma: bool = True, cluster: bool = True, idx16: bool = True,
-                 flow: bool = True):
+                 flow: bool = False):
         self._lib = _lib.load()
         interior = _as(interior, np.int64)
         weights = _as(weights, np.float64)
@@ -183,8 +183,8 @@ class Plan:
             flags |= _lib.RBF_NO_CLUSTER
         if not idx16:
             flags |= _lib.RBF_NO_IDX16
-        if not flow:
-            flags |= _lib.RBF_NO_FLOW
+        if flow:
+            flags |= _lib.RBF_FLOW
         handle = ctypes.c_void_p()
         rc = self._lib.rbf_plan_create(
             ctypes.byref(handle), int(n_total), int(n_rows), int(n), _ptr(interior), _ptr(rows),

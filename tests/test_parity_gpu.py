@@ -374,7 +374,7 @@ def test_flow_loop_failure_replays_the_exact_step(synth_cache):
     nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
     interior = shapes.interior_nodes
     plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
-                rb.forcing(nodes.positions[interior]))
+                rb.forcing(nodes.positions[interior]), flow=True)
     assert plan.info()["flow"] == 1
     dt = 40.0 * rb.stability_bound(shapes)
     want = orc.run_time_loop(nodes, shapes, dt=dt, steps=200)
@@ -394,11 +394,18 @@ def test_flow_loop_failure_replays_the_exact_step(synth_cache):
 @pytest.mark.parametrize("steps", [2, 3, 64, 65, 129])
 def test_flow_loop_step_counts(synth_cache, steps):
     nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
+    interior = shapes.interior_nodes
     want = orc.run_time_loop(nodes, shapes, steps=steps)
-    cfg = rb.SolveConfig(degree=2, support_size=15, nodes=200_000, steps=steps)
-    rep = rb.run_time_loop(cfg, nodes, shapes)
-    assert np.array_equal(rep.field, want["field"]) and rep.residual == want["residual"]
-    assert rep.steps == steps
+    for idx16 in (True, False):
+        plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                    rb.forcing(nodes.positions[interior]), nodes.positions, renumber=True,
+                    flow=True, idx16=idx16)
+        assert plan.info()["flow"] == 1
+        plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
+        res = plan.run(0.5 * rb.stability_bound(shapes), steps=steps)
+        assert np.array_equal(plan.get_field(), want["field"]) and res.residual == want["residual"]
+        assert res.steps_done == steps
+        plan.close()
 
 
 def test_idx16_overflow_slices_path(synth_cache, monkeypatch):
