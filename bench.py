@@ -286,7 +286,7 @@ def main():
             extra = int(min(200_000, max(1, args.steps * (1.0 / max(res.device_seconds, 1e-6)))))
             plan.run(dt, steps=extra)
     gpu_launches = plan.info()["launches"] - launches0  # includes the clock-keepalive run
-    gpu_launches = args.steps if info["resident"] == 0 else 1
+    gpu_launches = args.steps if info["resident"] == 0 else 1  # resident / cluster loop: one launch
     t = res.device_seconds
     value = args.steps * N_i / t
     bytes_per_step = info["bytes_per_step"]
@@ -344,7 +344,8 @@ def main():
                    f"working set {bytes_per_step / 1e6:.1f} MB fits L2 (no flush)"),
             "loop": {0: "resident on-chip loop (one CTA)",
                      1: "streaming step (plain loads), CUDA graphs of 64 steps",
-                     2: "streaming step (TMA bulk-copy ring, warp-specialised), CUDA graphs of 64 steps"}[
+                     2: "streaming step (TMA bulk-copy ring, warp-specialised), CUDA graphs of 64 steps",
+                     3: "cluster-resident loop (thread-block cluster, DSMEM halo, one launch)"}[
                          info["variant"]] + ("" if args.no_pdl or info["resident"] else " + PDL"),
             "parallelism": "single GPU",
         },
@@ -359,6 +360,12 @@ def main():
             "bytes_formula": "N_i*(12n+24): 8n w + 4n ids + 8 f + 8 u_self + 8 u_out",
             "peak_source": peak_src,
             "frac_of_8TBps_spec": achieved_gbs / 8000.0,
+            # with 16-bit two-window ids the step streams fewer bytes than B(n)
+            # (report compression separately from the B(n) fraction)
+            "index_bits": info["index_bits"],
+            "stream_bytes_per_launch": info["stream_bytes_per_step"],
+            "stream_achieved": info["stream_bytes_per_step"] / per_launch / 1e9,
+            "stream_frac": info["stream_bytes_per_step"] / per_launch / 1e9 / peak,
         },
         "e2e": {"value": e2e_value, "unit": "node-updates/s",
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,

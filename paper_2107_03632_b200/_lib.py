@@ -89,6 +89,8 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
+    if path is None and os.environ.get("RBFFD_LIB"):  # experiments: an alternative build
+        path = os.environ["RBFFD_LIB"]
     p = Path(path) if path is not None else LIB_PATH
     if not p.exists():
         raise OSError(
@@ -141,7 +143,7 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if path is None:
+    if path is None or os.environ.get("RBFFD_LIB") == str(path):
         _lib = lib
     return lib
 

@@ -72,8 +72,9 @@ struct KernelSet {
   static StreamFn stream() { return rbf::step_stream_kernel<NJ>; }
   static ResidentFn resident() { return rbf::resident_loop_kernel<NJ>; }
   static ClusterFn cluster() { return rbf::cluster_loop_kernel<NJ>; }
-  // consumer warps: 15 (512-thread CTA, <=128 regs) for narrow stencils, 8
-  // (<=168 regs) for wide ones whose NJ gathers need the registers
+  // consumer warps: 15 (512-thread CTA, <= 128 registers) for narrow
+  // stencils; 8 (<= 168 registers) for wide ones, which keep all NJ gathers in
+  // flight (measured 1 % faster at n=56 than 15 warps gathering in two halves)
   static constexpr int kCW = NJ <= 32 ? 15 : 8;
   static TmaFn tma(int rpl_req, bool idx16) {
     if constexpr (NJ > 0) {
@@ -858,7 +859,10 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
     int kn, r1, c1;
     pick_kernels(n, 1, false, &sf, &rf, &tf, &kn, &r1, &c1);
     const char* e = std::getenv("RBFFD_IDX16");
-    if (tf && N_i >= 4096 && !(flags & RBF_NO_IDX16) && !(flags & RBF_STREAM_LDG) &&
+    // wide stencils (n > 32) run consumer-bound: the decode costs more than
+    // the saved bytes (C4: 9.40e9 vs 9.72e9 upd/s, profiles/README.md)
+    const bool want16 = (n <= 32) || (e && std::atoi(e) == 2);
+    if (tf && want16 && N_i >= 4096 && !(flags & RBF_NO_IDX16) && !(flags & RBF_STREAM_LDG) &&
         !(e && std::atoi(e) == 0)) {
       RBF_TRY(dev_alloc(p.get(), &p->C16, sell));
       RBF_TRY(dev_alloc(p.get(), &p->meta, static_cast<size_t>(p->S)));

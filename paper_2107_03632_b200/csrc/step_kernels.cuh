@@ -489,60 +489,62 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
       mbar_wait(&full[s], static_cast<uint32_t>((i / stages) & 1));
       const unsigned char* base = ring + static_cast<size_t>(s) * stage_bytes;
       const long long slice0 = (g.contig ? blockIdx.x * cpc + i : blockIdx.x + i * gridDim.x) * sps + slot0;
-      bool live[RPL];
-      double g[RPL][NJ];
-      double u_self[RPL];
+      {
+        bool live[RPL];
+        double g[RPL][NJ];
+        double u_self[RPL];
 #pragma unroll
-      for (int t = 0; t < RPL; ++t) {
-        const long long r = (slice0 + t) * 32 + lane;
-        live[t] = (slice0 + t) < S && r < a.n_rows;
-        if (live[t]) {
-          // ids from the ring -> gathers, all issued before the first use
-          int c0;
-          if constexpr (IB == 2) {
-            const int4 m = reinterpret_cast<const int4*>(base + wbytes + cbytes + sps * 32 * 8)[slot0 + t];
-            if (m.z) {
-              const unsigned short* sC =
-                  reinterpret_cast<const unsigned short*>(base + wbytes) + (slot0 + t) * NJ * 32;
-              c0 = decode_id(sC[lane], m);
+        for (int t = 0; t < RPL; ++t) {
+          const long long r = (slice0 + t) * 32 + lane;
+          live[t] = (slice0 + t) < S && r < a.n_rows;
+          if (live[t]) {
+            // ids from the ring -> gathers, all issued before the first use
+            int c0;
+            if constexpr (IB == 2) {
+              const int4 m = reinterpret_cast<const int4*>(base + wbytes + cbytes + sps * 32 * 8)[slot0 + t];
+              if (m.z) {
+                const unsigned short* sC =
+                    reinterpret_cast<const unsigned short*>(base + wbytes) + (slot0 + t) * NJ * 32;
+                c0 = decode_id(sC[lane], m);
+                g[t][0] = ld_field(u_in + c0);
+#pragma unroll
+                for (int j = 1; j < NJ; ++j) g[t][j] = ld_field(u_in + decode_id(sC[j * 32 + lane], m));
+              } else {  // slice too spread for two 15-bit windows: int32 ids from HBM
+                const int* gC = a.C + (slice0 + t) * NJ * 32 + lane;
+                c0 = __ldg(gC);
+                g[t][0] = ld_field(u_in + c0);
+#pragma unroll
+                for (int j = 1; j < NJ; ++j) g[t][j] = ld_field(u_in + __ldg(gC + 32 * j));
+              }
+            } else {
+              const int* sC = reinterpret_cast<const int*>(base + wbytes) + (slot0 + t) * NJ * 32;
+              c0 = sC[lane];
               g[t][0] = ld_field(u_in + c0);
 #pragma unroll
-              for (int j = 1; j < NJ; ++j) g[t][j] = ld_field(u_in + decode_id(sC[j * 32 + lane], m));
-            } else {  // slice too spread for two 15-bit windows: int32 ids from HBM
-              const int* gC = a.C + (slice0 + t) * NJ * 32 + lane;
-              c0 = __ldg(gC);
-              g[t][0] = ld_field(u_in + c0);
-#pragma unroll
-              for (int j = 1; j < NJ; ++j) g[t][j] = ld_field(u_in + __ldg(gC + 32 * j));
+              for (int j = 1; j < NJ; ++j) g[t][j] = ld_field(u_in + sC[j * 32 + lane]);
             }
-          } else {
-            const int* sC = reinterpret_cast<const int*>(base + wbytes) + (slot0 + t) * NJ * 32;
-            c0 = sC[lane];
-            g[t][0] = ld_field(u_in + c0);
-#pragma unroll
-            for (int j = 1; j < NJ; ++j) g[t][j] = ld_field(u_in + sC[j * 32 + lane]);
+            // stencils list the centre first (neighborhoods.py:29-32): reuse it
+            const long long node = a.dst_base + r;
+            u_self[t] = (c0 == node) ? g[t][0] : ld_field(u_in + node);
           }
-          // stencils list the centre first (neighborhoods.py:29-32): reuse it
-          const long long node = a.dst_base + r;
-          u_self[t] = (c0 == node) ? g[t][0] : ld_field(u_in + node);
         }
-      }
 #pragma unroll
-      for (int t = 0; t < RPL; ++t) {
-        if (!live[t]) continue;
-        const long long r = (slice0 + t) * 32 + lane;
-        const double* sW = reinterpret_cast<const double*>(base) + (slot0 + t) * NJ * 32;
-        const double* sF = reinterpret_cast<const double*>(base + wbytes + cbytes) + (slot0 + t) * 32;
-        double acc = 0.0;  // weights read from the ring inside the serial chain
+        for (int t = 0; t < RPL; ++t) {
+          if (!live[t]) continue;
+          const long long r = (slice0 + t) * 32 + lane;
+          const double* sW = reinterpret_cast<const double*>(base) + (slot0 + t) * NJ * 32;
+          const double* sF = reinterpret_cast<const double*>(base + wbytes + cbytes) + (slot0 + t) * 32;
+          double acc = 0.0;  // weights read from the ring inside the serial chain
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(sW[j * 32 + lane], g[t][j]));
-        const double value = __dadd_rn(u_self[t], __dmul_rn(dt, __dadd_rn(sF[lane], acc)));
-        u_out[a.dst_base + r] = value;
-        if (!isfinite(value)) bad = true;
-        if (flags & kNeedResidual) {
-          const unsigned long long b = static_cast<unsigned long long>(
-              __double_as_longlong(fabs(__dsub_rn(value, u_self[t]))));
-          dmax = b > dmax ? b : dmax;
+          for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(sW[j * 32 + lane], g[t][j]));
+          const double value = __dadd_rn(u_self[t], __dmul_rn(dt, __dadd_rn(sF[lane], acc)));
+          u_out[a.dst_base + r] = value;
+          if (!isfinite(value)) bad = true;
+          if (flags & kNeedResidual) {
+            const unsigned long long b = static_cast<unsigned long long>(
+                __double_as_longlong(fabs(__dsub_rn(value, u_self[t]))));
+            dmax = b > dmax ? b : dmax;
+          }
         }
       }
       // unit fully consumed: hand it back to the producer (the arrive has
