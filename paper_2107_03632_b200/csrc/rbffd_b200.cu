@@ -904,12 +904,18 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   }
   // cluster-resident loop: rows spread over Q SMs of one cluster (DSMEM halo)
   if (!(flags & RBF_NO_RESIDENT) && !(flags & RBF_NO_CLUSTER) && N_i >= 256) {
-    int q = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(2, (N_i + 63) / 64)));
+    // 8 CTAs measured best on the paper's Fig. 1 case (1.30 us/step vs 1.51 at
+    // 16, profiles/README.md); more only when a CTA's rows would not fit
+    const size_t NU = static_cast<size_t>(((B + 1) & ~int64_t(1)) + N_i + 2);
+    auto smem_for = [&](int qq) {
+      const int rpc_ = static_cast<int>(((N_i + qq - 1) / qq + 1) & ~int64_t(1));
+      return 2 * NU * 8 + 2 * 16 * 2 * 8 + static_cast<size_t>(n) * rpc_ * 12 + rpc_ * 8 + rpc_ * 4;
+    };
+    int q = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(2, (N_i + 63) / 64)));
+    while (q < 16 && smem_for(q) > 200 * 1024) ++q;
     if (const char* e = std::getenv("RBFFD_CLUSTER")) q = std::max(2, std::min(16, std::atoi(e)));
     const int rpc = static_cast<int>(((N_i + q - 1) / q + 1) & ~int64_t(1));
-    const int rp = rpc;
-    const size_t NU = static_cast<size_t>(((B + 1) & ~int64_t(1)) + N_i + 2);
-    const size_t csmem = 2 * NU * 8 + 2 * 16 * 2 * 8 + static_cast<size_t>(n) * rp * 12 + rp * 8 + rp * 4;
+    const size_t csmem = smem_for(q);
     ClusterFn cfn = nullptr;
     switch (n) {
 #define RBF_CCASE(K) \
