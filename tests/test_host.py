@@ -2,6 +2,8 @@
 config validation, Dirichlet values, forcing, norms, stability bound -- each
 checked against the reference's expressions / golden values."""
 
+import csv
+
 import numpy as np
 import pytest
 
@@ -79,3 +81,44 @@ def test_synthetic_domain_shape():
     rows = st.neighbors[sh.interior_nodes]
     vals = (nodes.positions[:, 0] ** 2 + nodes.positions[:, 1] ** 2)[rows]
     assert np.allclose(np.einsum("ij,ij->i", sh.weights, vals), 4.0, rtol=1e-6)
+
+
+def test_benchmark_csv_and_speedup(tmp_path):
+    """perf.py:110-114, :160-170 (test_perf.py:82-89, :134-142)."""
+    from paper_2107_03632_b200 import perf
+
+    r = perf.TimingReport.from_run(1000, 900, 15, 2, 10, 1, 0.5, np.zeros(1000))
+    assert r.ns_per_step_node == pytest.approx(1e9 * 0.5 / (10 * 900))
+    path = tmp_path / "benchmark.csv"
+    perf.save_benchmark_csv([r], path)
+    rows = list(csv.reader(open(path)))
+    assert rows[0] == ["N", "n", "m", "threads", "steps", "loop_seconds", "ns_per_step_node"]
+    assert int(rows[1][0]) == 1000
+    assert perf.speedup(10.0, 2.0) == 5.0
+    with pytest.raises(rb.ParameterError):
+        perf.speedup(0.0, 1.0)
+
+
+def test_solution_csv_and_report_json(tmp_path, golden):
+    """solver.py:262-277 (test_solver.py:321-342) on a recorded golden field."""
+    import json
+
+    nodes, _, _, z = golden("small")
+    field = z["fixed50__field"]
+    linf, l2 = rb.error_norms(field, nodes)
+    rep = rb.SolveReport(field=field, steps=50, wall_time_s=0.01, linf=linf, l2=l2,
+                         residual=1.5, config=rb.SolveConfig(nodes=300, support_size=12,
+                                                             dt=1e-4, steps=50).as_dict())
+    path = tmp_path / "solution.csv"
+    rb.save_solution_csv(nodes, rep.field, path)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "x,y,kind,u,exact,abs_error"
+    assert len(lines) == nodes.n_total + 1
+    cells = lines[1].split(",")
+    assert cells[2] in ("interior", "boundary")
+    assert float(cells[5]) == abs(float(cells[3]) - float(cells[4]))
+    jpath = tmp_path / "report.json"
+    rb.save_report_json(rep, jpath)
+    loaded = json.loads(jpath.read_text())
+    assert set(loaded) == {"steps", "wall_time_s", "linf", "l2", "residual", "config"}
+    assert loaded["steps"] == 50 and loaded["config"]["m"] == 2
