@@ -230,6 +230,8 @@ def main():
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the multi-rank (torchrun/NCCL) path even with one rank (testing)")
     ap.add_argument("--quick", action="store_true",
                     help="profiling mode: timed region only (no e2e, clock keep-alive, CPU leg)")
     args = ap.parse_args()
@@ -241,7 +243,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or args.force_dist:
         from paper_2107_03632_b200 import multigpu
 
         return multigpu.bench_main(args, METRIC, WORKLOADS)

@@ -79,6 +79,8 @@ struct rbf_group {
   cudaStream_t stream = nullptr;  // every launch of the group runs here
   rbf::DevStatus** d_status = nullptr;  // device array of the parts' status pointers
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaGraphExec_t fast_graph = nullptr;  // kGroupGraph fixed-mode steps (pack, exchange, step)
+  long long* d_red = nullptr;            // [2] end-of-run reduction: {first bad step key, residual bits}
 };
 
 namespace {
@@ -155,6 +157,91 @@ int group_step_kernel(rbf_group* g, rbf_plan* p, int cur, int flags) {
   p->stream = saved;
   p->pdl = pdl;
   return rc;
+}
+
+constexpr int kGroupGraph = 64;  // even: buffer parity is static inside the graph
+
+// One fixed-mode step of every local part without a per-step reduction: each
+// part's step kernel keeps its own first bad step and (on the last step) its
+// residual max in its status, like a single-plan run.
+int group_fast_step(rbf_group* g, int cur, int flags) {
+  for (rbf_plan* p : g->parts) RBF_TRY(group_pack(g, p, cur));
+  RBF_TRY(group_exchange(g, cur));
+  for (rbf_plan* p : g->parts) RBF_TRY(group_step_kernel(g, p, cur, flags));
+  return RBF_OK;
+}
+
+int group_fast_graph(rbf_group* g, cudaGraphExec_t* out) {
+  if (g->fast_graph) {
+    *out = g->fast_graph;
+    return RBF_OK;
+  }
+  RBF_CK(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = RBF_OK;
+  for (int i = 0; i < kGroupGraph && rc == RBF_OK; ++i) rc = group_fast_step(g, i & 1, 0);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(g->stream, &graph);
+  if (rc != RBF_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (e != cudaSuccess) return fail(RBF_ERR_CUDA, std::string("group graph capture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&g->fast_graph, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(RBF_ERR_CUDA, std::string("group graph instantiate: ") + cudaGetErrorString(e));
+  *out = g->fast_graph;
+  return RBF_OK;
+}
+
+// Fixed-mode run without per-step reductions.  On return *any_bad tells the
+// caller to restore the start field and replay on the exact per-step path.
+int group_run_fast(rbf_group* g, int64_t limit, bool* any_bad, unsigned long long* res_bits) {
+  *any_bad = false;
+  for (rbf_plan* p : g->parts) {
+    if (!p->u_init) RBF_TRY(dev_alloc(p, &p->u_init, static_cast<size_t>(p->N)));
+    RBF_CK(cudaMemcpyAsync(p->u_init, p->U[0], sizeof(double) * p->N, cudaMemcpyDeviceToDevice, g->stream));
+  }
+  cudaGraphExec_t graph = nullptr;
+  if (limit > kGroupGraph) RBF_TRY(group_fast_graph(g, &graph));
+  RBF_CK(cudaEventRecord(g->ev0, g->stream));
+  const int64_t chunks = (limit - 1) / kGroupGraph;
+  for (int64_t c = 0; c < chunks; ++c) RBF_CK(cudaGraphLaunch(graph, g->stream));
+  for (int64_t s = chunks * kGroupGraph; s < limit; ++s)
+    RBF_TRY(group_fast_step(g, static_cast<int>(s & 1), s == limit - 1 ? rbf::kNeedResidual : 0));
+  RBF_CK(cudaEventRecord(g->ev1, g->stream));
+  for (rbf_plan* p : g->parts) p->launches += 2 * limit;
+  // end-of-run reduction over all parts: min first-bad-step, max residual bits
+  if (!g->d_red) RBF_CK(cudaMalloc(&g->d_red, 2 * sizeof(long long)));
+  long long key = std::numeric_limits<long long>::max();
+  unsigned long long bits = 0;
+  RBF_CK(cudaStreamSynchronize(g->stream));
+  for (rbf_plan* p : g->parts) {
+    RBF_TRY(read_status(p));
+    if (p->h_st->bad_step >= 0) key = std::min<long long>(key, p->h_st->bad_step);
+    if (p->h_st->last_res_step == limit - 1) bits = std::max<unsigned long long>(bits, p->h_st->last_res_bits);
+  }
+  if (g->nccl) {
+    long long h[2] = {key, static_cast<long long>(bits)};
+    RBF_CK(cudaMemcpyAsync(g->d_red, h, sizeof(h), cudaMemcpyHostToDevice, g->stream));
+    RBF_NCK(g_nccl.GroupStart());
+    RBF_NCK(g_nccl.AllReduce(g->d_red, g->d_red, 1, ncclInt64, ncclMin, g->comm, g->stream));
+    RBF_NCK(g_nccl.AllReduce(g->d_red + 1, g->d_red + 1, 1, ncclUint64, ncclMax, g->comm, g->stream));
+    RBF_NCK(g_nccl.GroupEnd());
+    RBF_CK(cudaMemcpyAsync(h, g->d_red, sizeof(h), cudaMemcpyDeviceToHost, g->stream));
+    RBF_CK(cudaStreamSynchronize(g->stream));
+    key = h[0];
+    bits = static_cast<unsigned long long>(h[1]);
+  }
+  *res_bits = bits;
+  if (key != std::numeric_limits<long long>::max()) {
+    *any_bad = true;
+    for (rbf_plan* p : g->parts) {
+      RBF_CK(cudaMemcpyAsync(p->U[0], p->u_init, sizeof(double) * p->N, cudaMemcpyDeviceToDevice, g->stream));
+      RBF_CK(cudaMemcpyAsync(p->U[1], p->u_init, sizeof(double) * p->N, cudaMemcpyDeviceToDevice, g->stream));
+    }
+    RBF_CK(cudaStreamSynchronize(g->stream));
+  }
+  return RBF_OK;
 }
 
 }  // namespace
@@ -257,6 +344,31 @@ int rbf_group_run(rbf_group* g, double dt, int64_t steps, int32_t mode, double t
     RBF_TRY(reset_status(p, dt, tol));
     RBF_CK(cudaStreamSynchronize(p->stream));
   }
+  if (!steady && limit >= 2 && !std::getenv("RBFFD_GROUP_EXACT")) {
+    bool any_bad = false;
+    unsigned long long bits = 0;
+    RBF_TRY(group_run_fast(g, limit, &any_bad, &bits));
+    if (!any_bad) {
+      float ms = 0.f;
+      RBF_CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+      for (rbf_plan* p : g->parts) p->cur = static_cast<int>(limit & 1);
+      double m;
+      std::memcpy(&m, &bits, sizeof(m));
+      if (device_seconds) *device_seconds = ms * 1e-3;
+      if (bad_step) *bad_step = -1;
+      if (steps_done) *steps_done = limit;
+      if (residual) *residual = m / dt;
+      if (has_residual) *has_residual = 1;
+      return RBF_OK;
+    }
+    // a non-finite value appeared: replay from the start field on the exact
+    // per-step path, which stops at the reference's step (solver.py:200-206)
+    for (rbf_plan* p : g->parts) {
+      p->cur = 0;
+      RBF_TRY(reset_status(p, dt, tol));
+      RBF_CK(cudaStreamSynchronize(p->stream));
+    }
+  }
   RBF_CK(cudaEventRecord(g->ev0, g->stream));
   constexpr int64_t kPoll = 64;
   for (int64_t s = 0; s < limit; ++s) {
@@ -311,8 +423,10 @@ void rbf_group_destroy(rbf_group* g) {
   if (!g) return;
   cudaSetDevice(g->device);
   if (g->stream) cudaStreamSynchronize(g->stream);
+  if (g->fast_graph) cudaGraphExecDestroy(g->fast_graph);
   if (g->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(g->comm);
   cudaFree(g->d_status);
+  cudaFree(g->d_red);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
   if (g->stream) cudaStreamDestroy(g->stream);

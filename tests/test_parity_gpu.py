@@ -477,6 +477,26 @@ def test_partitioned_group_matches_reference(golden, manifest, name, case, P):
     group.close()
 
 
+@pytest.mark.parametrize("exact", [False, True], ids=["fast", "per-step-reduce"])
+def test_partitioned_group_paths(golden, manifest, monkeypatch, exact):
+    """Fixed mode runs without per-step reductions (one reduction at the end,
+    exact replay on failure); RBFFD_GROUP_EXACT forces the per-step path."""
+    from paper_2107_03632_b200.multigpu import LocalGroup, partition, run_partitioned
+
+    if exact:
+        monkeypatch.setenv("RBFFD_GROUP_EXACT", "1")
+    for name, case, P in (("m4", "fixed200", 3), ("crit6", "fixed100", 4)):
+        nodes, _, shapes, z = golden(name)
+        meta = manifest[name][case]
+        interior = shapes.interior_nodes
+        parts = partition(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                          rb.forcing(nodes.positions[interior]), nodes.positions, P)
+        group = LocalGroup(parts)
+        field, steps, residual, _, _ = run_partitioned(group, nodes, shapes, config_for(nodes, shapes, meta))
+        assert np.array_equal(field, z[f"{case}__field"]) and residual == meta["residual"]
+        group.close()
+
+
 def test_partitioned_group_instability_and_synthetic(golden, synth_cache):
     from paper_2107_03632_b200.multigpu import LocalGroup, partition, run_partitioned
 
