@@ -124,9 +124,10 @@ int group_exchange(rbf_group* g, int cur) {
         if (q->halo_peers[k] == g->ids[a]) j = static_cast<int>(k);
       if (j < 0 || q->halo_send_count[j] != p->halo_recv_count[i])
         return fail(RBF_ERR_PARAM, "halo lists of two parts disagree");
-      RBF_CK(cudaMemcpyPeerAsync(p->U[cur] + p->halo_recv_off[i], p->device,
-                                 q->halo_sendbuf + q->halo_send_off[j], q->device,
-                                 sizeof(double) * p->halo_recv_count[i], g->stream));
+      // parts of an in-process group share one device (rbf_group_create):
+      // a plain device-to-device copy, capturable into the step graph
+      RBF_CK(cudaMemcpyAsync(p->U[cur] + p->halo_recv_off[i], q->halo_sendbuf + q->halo_send_off[j],
+                             sizeof(double) * p->halo_recv_count[i], cudaMemcpyDeviceToDevice, g->stream));
     }
   }
   return RBF_OK;
