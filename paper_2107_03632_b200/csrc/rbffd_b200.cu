@@ -71,7 +71,9 @@ template <int NJ>
 struct KernelSet {
   static StreamFn stream() { return rbf::step_stream_kernel<NJ>; }
   static ResidentFn resident() { return rbf::resident_loop_kernel<NJ>; }
-  static ClusterFn cluster() { return rbf::cluster_loop_kernel<NJ>; }
+  static ClusterFn cluster(bool small) {
+    return small ? rbf::cluster_loop_kernel<NJ, 256> : rbf::cluster_loop_kernel<NJ, 1024>;
+  }
   // consumer warps: 15 (512-thread CTA, <= 128 registers) for narrow
   // stencils; 8 (<= 168 registers) for wide ones, which keep all NJ gathers in
   // flight (measured 1 % faster at n=56 than 15 warps gathering in two halves)
@@ -543,6 +545,14 @@ int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
     a.flags = steady ? rbf::kSteady : 0;
     a.rpc = p->cluster_rpc;
     a.st = p->st;
+    a.phase_cycles = nullptr;
+    static unsigned long long* d_phase = nullptr;  // RBFFD_CLUSTER_PHASES=1: per-phase cycles to stderr
+    const bool phases = std::getenv("RBFFD_CLUSTER_PHASES") != nullptr;
+    if (phases) {
+      if (!d_phase) RBF_CK(cudaMalloc(&d_phase, 4 * sizeof(unsigned long long)));
+      RBF_CK(cudaMemsetAsync(d_phase, 0, 4 * sizeof(unsigned long long), p->stream));
+      a.phase_cycles = d_phase;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p->cluster_q);
     cfg.blockDim = dim3(p->cluster_threads);
@@ -557,6 +567,14 @@ int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
     cfg.numAttrs = 1;
     RBF_CK(cudaLaunchKernelEx(&cfg, p->cluster_fn, a));
     ++p->launches;
+    if (phases) {
+      unsigned long long h[4];
+      RBF_CK(cudaMemcpyAsync(h, d_phase, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
+      RBF_CK(cudaStreamSynchronize(p->stream));
+      std::fprintf(stderr, "[rbffd] cluster q=%d cycles/step: compute %.0f partials %.0f barrier %.0f decide %.0f\n",
+                   p->cluster_q, double(h[0]) / limit, double(h[1]) / limit, double(h[2]) / limit,
+                   double(h[3]) / limit);
+    }
   } else if (limit > 0 && p->N_i > 0) {
     rbf::ResidentArgs a;
     a.W = p->W;
@@ -904,14 +922,15 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   }
   // cluster-resident loop: rows spread over Q SMs of one cluster (DSMEM halo)
   if (!(flags & RBF_NO_RESIDENT) && !(flags & RBF_NO_CLUSTER) && N_i >= 256) {
-    // 8 CTAs measured best on the paper's Fig. 1 case (1.30 us/step vs 1.51 at
-    // 16, profiles/README.md); more only when a CTA's rows would not fit
+    // 4-8 CTAs measured best on the paper's Fig. 1 case (1.01 / 1.04 us/step vs
+    // 1.30 at 16, profiles/README.md); more when a CTA would own more than 256
+    // rows (register-resident variant) or its rows would not fit
     const size_t NU = static_cast<size_t>(((B + 1) & ~int64_t(1)) + N_i + 2);
     auto smem_for = [&](int qq) {
       const int rpc_ = static_cast<int>(((N_i + qq - 1) / qq + 1) & ~int64_t(1));
-      return 2 * NU * 8 + 2 * 16 * 2 * 8 + static_cast<size_t>(n) * rpc_ * 12 + rpc_ * 8 + rpc_ * 4;
+      return 2 * NU * 8 + 2 * 16 * 32 * 2 * 8 + static_cast<size_t>(n) * rpc_ * 12 + rpc_ * 8 + rpc_ * 4;
     };
-    int q = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(2, (N_i + 63) / 64)));
+    int q = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(4, (N_i + 255) / 256)));
     while (q < 16 && smem_for(q) > 200 * 1024) ++q;
     if (const char* e = std::getenv("RBFFD_CLUSTER")) q = std::max(2, std::min(16, std::atoi(e)));
     const int rpc = static_cast<int>(((N_i + q - 1) / q + 1) & ~int64_t(1));
@@ -920,15 +939,15 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
     switch (n) {
 #define RBF_CCASE(K) \
   case K:            \
-    cfn = KernelSet<K>::cluster(); \
+    cfn = KernelSet<K>::cluster(rpc <= 256); \
     break;
       RBF_SPECIALISED(RBF_CCASE)
 #undef RBF_CCASE
       default:
-        cfn = KernelSet<0>::cluster();
+        cfn = KernelSet<0>::cluster(rpc <= 256);
     }
     const int threads = std::min(1024, ((rpc + 31) / 32) * 32);
-    if (csmem <= 200 * 1024 &&
+    if (csmem <= 200 * 1024 && rpc <= 1024 &&
         set_max_smem(cfn) == cudaSuccess &&
         (q <= 8 || cudaFuncSetAttribute(cfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
       cudaLaunchConfig_t cfg = {};

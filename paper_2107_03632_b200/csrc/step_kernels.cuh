@@ -725,13 +725,18 @@ struct ClusterArgs {
   long long n_rows, N, dst_base, limit;
   int n, flags, rpc;        // rows per CTA (even)
   DevStatus* st;
+  unsigned long long* phase_cycles;  // optional [4]: compute / partials / cluster barrier / decide (CTA 0)
 };
 
-template <int NJ>
-__global__ void __launch_bounds__(1024, 1) cluster_loop_kernel(ClusterArgs a) {
+template <int NJ, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) cluster_loop_kernel(ClusterArgs a) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char cl_smem[];
+  // narrow stencils in <=256-thread CTAs keep their row's weights / ids in
+  // registers (one row per thread); otherwise they are read from shared memory
+  constexpr bool kReg = NJ > 0 && NJ <= 32 && MAXT <= 256;
+  constexpr int KR = kReg ? NJ : 1;
   const int n = NJ > 0 ? NJ : a.n;
   const int q = static_cast<int>(cluster.block_rank());
   const int Q = static_cast<int>(cluster.num_blocks());
@@ -742,16 +747,16 @@ __global__ void __launch_bounds__(1024, 1) cluster_loop_kernel(ClusterArgs a) {
   const int r1 = min(static_cast<int>(a.n_rows), r0 + a.rpc);
   const int nr = max(0, r1 - r0);
   const int rp = (a.rpc + 1) & ~1;
-  // smem: U[2][NU] | red[2][16][2] u64 | W[n][rp] | F[rp] | C[n][rp] | mask[rp] (u32)
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = (nt + 31) >> 5;
+  // smem: U[2][NU] | red[2][16*32][2] u64 | W[n][rp] | F[rp] | C[n][rp] | mask[rp] (u32)
   double* U = reinterpret_cast<double*>(cl_smem);
   unsigned long long* red = reinterpret_cast<unsigned long long*>(U + 2 * NU);
-  double* sW = reinterpret_cast<double*>(red + 2 * 16 * 2);
+  const int slots = Q * nwarps;  // partials: one slot per (CTA, warp)
+  double* sW = reinterpret_cast<double*>(red + 2 * 16 * 32 * 2);
   double* sF = sW + static_cast<size_t>(n) * rp;
   int* sC = reinterpret_cast<int*>(sF + rp);
   unsigned int* sM = reinterpret_cast<unsigned int*>(sC + static_cast<size_t>(n) * rp);
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = (nt + 31) >> 5;
-  __shared__ unsigned long long s_part[32][2];
 
   for (int i = tid; i < static_cast<int>(a.N); i += nt) {
     const int li = i < B ? i : i - B + IB;
@@ -770,7 +775,23 @@ __global__ void __launch_bounds__(1024, 1) cluster_loop_kernel(ClusterArgs a) {
     sF[k] = a.F[r];
     sM[k] = a.dest[r];
   }
-  for (int i = tid; i < 2 * 16 * 2; i += nt) red[i] = 0ull;
+  for (int i = tid; i < 2 * 16 * 32 * 2; i += nt) red[i] = 0ull;
+  __syncthreads();
+  // this thread's row in registers (kReg: requires nr <= blockDim, host-checked)
+  double wr[KR];
+  int cr[KR];
+  double fr = 0.0;
+  unsigned int mr = 0;
+  const bool own = tid < nr;
+  if (kReg && own) {
+#pragma unroll
+    for (int j = 0; j < KR; ++j) {
+      wr[j] = sW[j * rp + tid];
+      cr[j] = sC[j * rp + tid];
+    }
+    fr = sF[tid];
+    mr = sM[tid];
+  }
   cluster.sync();
 
   DevStatus* st = a.st;
@@ -779,66 +800,90 @@ __global__ void __launch_bounds__(1024, 1) cluster_loop_kernel(ClusterArgs a) {
   long long step = 0, bad_step = -1, conv_step = -1, last_res_step = -1;
   unsigned long long last_bits = 0;
   int cur = 0;
+  long long t_a = 0, t_b = 0, t_c = 0, t_d = 0;
+  const bool timed = a.phase_cycles != nullptr && q == 0 && tid == 0;
   for (; step < a.limit; ++step) {
+    const long long t0 = timed ? clock64() : 0;
     const int nxt = cur ^ 1;
     const bool need_res = steady || step == a.limit - 1;
     const double* uc = U + cur * NU;
     double* un = U + nxt * NU;
     bool bad = false;
     unsigned long long dmax = 0ull;
-    for (int k = tid; k < nr; k += nt) {
-      double acc = 0.0;
-      if constexpr (NJ > 0) {
+    if constexpr (kReg) {
+      if (own) {
+        double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(sW[j * rp + k], uc[sC[j * rp + k]]));
-      } else {
+        for (int j = 0; j < KR; ++j) acc = __dadd_rn(acc, __dmul_rn(wr[j], uc[cr[j]]));
+        const int li = IB + r0 + tid;
+        const double u_self = uc[li];
+        const double value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(fr, acc)));
+        un[li] = value;
+        unsigned int m = mr;
+        while (m) {  // push to the CTAs that read this node
+          const int dq = __ffs(m) - 1;
+          m &= m - 1;
+          *cluster.map_shared_rank(un + li, dq) = value;
+        }
+        bad = !isfinite(value);
+        if (need_res)
+          dmax = static_cast<unsigned long long>(__double_as_longlong(fabs(__dsub_rn(value, u_self))));
+      }
+    } else {
+      for (int k = tid; k < nr; k += nt) {
+        double acc = 0.0;
         for (int j = 0; j < n; ++j) acc = __dadd_rn(acc, __dmul_rn(sW[j * rp + k], uc[sC[j * rp + k]]));
-      }
-      const int li = IB + r0 + k;
-      const double u_self = uc[li];
-      const double value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(sF[k], acc)));
-      un[li] = value;
-      unsigned int m = sM[k];
-      while (m) {  // push to the CTAs that read this node
-        const int dq = __ffs(m) - 1;
-        m &= m - 1;
-        *cluster.map_shared_rank(un + li, dq) = value;
-      }
-      bad |= !isfinite(value);
-      if (need_res) {
-        const unsigned long long b =
-            static_cast<unsigned long long>(__double_as_longlong(fabs(__dsub_rn(value, u_self))));
-        dmax = b > dmax ? b : dmax;
-      }
-    }
-    // CTA partials -> every CTA's slot [nxt][q]
-    unsigned long long wm = warp_max_u64(dmax);
-    const unsigned int wb = __any_sync(0xffffffffu, bad) ? 1u : 0u;
-    if (lane == 0) {
-      s_part[warp][0] = wm;
-      s_part[warp][1] = wb;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      unsigned long long m0 = 0, m1 = 0;
-      for (int w = 0; w < nwarps; ++w) {
-        m0 = s_part[w][0] > m0 ? s_part[w][0] : m0;
-        m1 |= s_part[w][1];
-      }
-      for (int dq = 0; dq < Q; ++dq) {
-        unsigned long long* slot = cluster.map_shared_rank(red + (nxt * 16 + q) * 2, dq);
-        slot[0] = m0;
-        slot[1] = m1;
+        const int li = IB + r0 + k;
+        const double u_self = uc[li];
+        const double value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(sF[k], acc)));
+        un[li] = value;
+        unsigned int m = sM[k];
+        while (m) {
+          const int dq = __ffs(m) - 1;
+          m &= m - 1;
+          *cluster.map_shared_rank(un + li, dq) = value;
+        }
+        bad |= !isfinite(value);
+        if (need_res) {
+          const unsigned long long b =
+              static_cast<unsigned long long>(__double_as_longlong(fabs(__dsub_rn(value, u_self))));
+          dmax = b > dmax ? b : dmax;
+        }
       }
     }
+    const long long t1 = timed ? clock64() : 0;
+    // warp partials -> slot (q, warp) of every CTA, one lane per destination.
+    // The residual max is only reduced on steps that need it (every step in
+    // steady mode, the last one in fixed mode, solver.py:208-211); the
+    // non-finite flag every step (solver.py:200).
+    const unsigned int wb = __reduce_or_sync(0xffffffffu, bad ? 1u : 0u);
+    const unsigned long long wm = need_res ? warp_max_u64(dmax) : 0ull;
+    if (lane < Q) {
+      unsigned long long* slot = cluster.map_shared_rank(red + (nxt * 16 * 32 + q * nwarps + warp) * 2, lane);
+      slot[0] = wm;
+      slot[1] = wb;
+    }
+    const long long t2 = timed ? clock64() : 0;
     cluster.sync();  // publishes the step: field values and partials
-    unsigned long long gmax = 0ull, gbad = 0ull;
-    for (int dq = 0; dq < Q; ++dq) {
-      const unsigned long long* slot = red + (nxt * 16 + dq) * 2;
-      gmax = slot[0] > gmax ? slot[0] : gmax;
-      gbad |= slot[1];
+    const long long t3 = timed ? clock64() : 0;
+    unsigned long long gmax = 0ull;
+    unsigned int lb = 0;
+    for (int e = lane; e < slots; e += 32) lb |= static_cast<unsigned int>(red[(nxt * 16 * 32 + e) * 2 + 1]);
+    const unsigned int gbad = __reduce_or_sync(0xffffffffu, lb);
+    if (need_res) {
+      for (int e = lane; e < slots; e += 32) {
+        const unsigned long long v = red[(nxt * 16 * 32 + e) * 2];
+        gmax = v > gmax ? v : gmax;
+      }
+      gmax = warp_max_u64(gmax);
     }
     cur = nxt;
+    if (timed) {
+      t_a += t1 - t0;
+      t_b += t2 - t1;
+      t_c += t3 - t2;
+      t_d += clock64() - t3;
+    }
     if (gbad) {
       bad_step = step;
       break;
@@ -852,6 +897,12 @@ __global__ void __launch_bounds__(1024, 1) cluster_loop_kernel(ClusterArgs a) {
         break;
       }
     }
+  }
+  if (timed) {
+    a.phase_cycles[0] = t_a;
+    a.phase_cycles[1] = t_b;
+    a.phase_cycles[2] = t_c;
+    a.phase_cycles[3] = t_d;
   }
   // the field after the last executed step (after a failure: its u2) is U[cur]
   const double* uf = U + cur * NU;
