@@ -524,3 +524,33 @@ def test_partitioned_group_instability_and_synthetic(golden, synth_cache):
     want = orc.run_time_loop(nodes, shapes, steps=50)
     assert np.array_equal(field, want["field"]) and residual == want["residual"]
     group.close()
+
+
+@pytest.mark.parametrize("n_rows", [1, 33, 100])
+def test_streaming_variants_on_tiny_row_counts(n_rows):
+    """Partial last slices and single-row problems through every loop variant."""
+    rng = np.random.default_rng(n_rows)
+    N = n_rows + 40
+    n = 15
+    interior = np.arange(40, N, dtype=np.int64)
+    rows = np.empty((n_rows, n), dtype=np.int64)
+    rows[:, 0] = interior
+    rows[:, 1:] = rng.integers(0, N, size=(n_rows, n - 1))
+    weights = rng.normal(size=(n_rows, n)) * 1e-2
+    f = rng.normal(size=n_rows)
+    u0 = rng.normal(size=N)
+    u2 = u0.copy()
+    want = u0.copy()
+    for _ in range(7):
+        step = want.copy()
+        orc.step_kernel(want, step, interior, rows, weights, f, 0.3)
+        want = step
+    for kw in (dict(), dict(cluster=False), dict(resident=False), dict(resident=False, tma=False),
+               dict(resident=False, pdl=False)):
+        plan = Plan(N, interior, rows, weights, f, **kw)
+        plan.set_field(u0)
+        res = plan.run(0.3, steps=7)
+        assert res.steps_done == 7
+        assert np.array_equal(plan.get_field(), want), kw
+        plan.close()
+    del u2
