@@ -110,6 +110,17 @@ int rbf_plan_create_assembled(rbf_plan** out, int64_t N, int64_t N_i, int32_t n,
  * solver.py:249-254), for plans whose weights never left the device. */
 int rbf_plan_weight_row_sum_max(rbf_plan* plan, double* out);
 
+/*
+ * Plan files (replacing the reference's CSV shape /
+ * stencil files, weights.py:209-215, neighborhoods.py:104-122, for the hot
+ * path): the packed device layout -- SELL weights and ids, forcing, 16-bit id
+ * windows, renumbering maps -- written once and loaded straight back into
+ * HBM, skipping validation, renumbering, packing and id compression.  A
+ * loaded plan runs bit-identically to the plan that was saved.
+ */
+int rbf_plan_save(const rbf_plan* plan, const char* path);
+int rbf_plan_load(rbf_plan** out, const char* path, int32_t device, uint32_t flags);
+
 /* Replace the per-row forcing (explicit_step's f[interior], solver.py:156). */
 int rbf_set_forcing(rbf_plan* plan, const double* f_int);
 

@@ -14,6 +14,8 @@ from .problem import (
     closed_form_solution,
     forcing,
     load_fixture,
+    load_problem,
+    save_problem,
     node_count_for_spacing,
     spacing_for_node_count,
 )

@@ -53,6 +53,8 @@ EXPORTED = (
     "rbf_assemble_weights",
     "rbf_plan_create_assembled",
     "rbf_plan_weight_row_sum_max",
+    "rbf_plan_save",
+    "rbf_plan_load",
 )
 
 
@@ -138,6 +140,8 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "rbf_assemble_weights": ([vp, i64, vp, i64, i32, i32, vp, pi64, i32], i32),
         "rbf_plan_create_assembled": ([ctypes.POINTER(vp), i64, i64, i32, i32, vp, vp, vp, vp, i32, u32], i32),
         "rbf_plan_weight_row_sum_max": ([vp, pdbl], i32),
+        "rbf_plan_save": ([vp, ctypes.c_char_p], i32),
+        "rbf_plan_load": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, u32], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -652,6 +652,231 @@ int launch_assemble(const double* d_pos, const int* d_rows, long long cnt, long 
   return RBF_OK;
 }
 
+// Kernel / loop selection shared by rbf_plan_create and rbf_plan_load: 16-bit
+// ids, the resident / cluster loops, the TMA ring geometry, the dataflow loop.
+int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
+  const int64_t N = p->N, N_i = p->N_i, B = p->B;
+  const int n = p->n;
+  const int device = p->device;
+  const size_t sell = static_cast<size_t>(p->S) * 32 * n;
+  // ---- kernel selection -----------------------------------------------------
+  int cw = 8;         // consumer warps of the TMA ring kernel (per width, KernelSet::kCW)
+  int rpl_req = 1;    // rows per lane of the TMA consumers (RBFFD_TMA_RPL=2: two, n <= 20)
+  if (const char* e = std::getenv("RBFFD_TMA_RPL")) rpl_req = std::atoi(e);
+  TmaFn tma_fn = nullptr;
+  int rpl = 1;
+  // 16-bit two-window ids for the TMA ring (only worth it when almost every
+  // slice fits; the rest fall back to int32 ids read from HBM)
+  bool idx16 = false;
+  {
+    StreamFn sf;
+    ResidentFn rf;
+    TmaFn tf = nullptr;
+    int kn, r1, c1;
+    pick_kernels(n, 1, false, &sf, &rf, &tf, &kn, &r1, &c1);
+    const char* e = std::getenv("RBFFD_IDX16");
+    // wide stencils (n > 32) run consumer-bound: the decode costs more than
+    // the saved bytes (C4: 9.40e9 vs 9.72e9 upd/s, profiles/README.md)
+    const bool want16 = (n <= 32) || (e && std::atoi(e) == 2);
+    if (p->C16) {  // loaded from a plan file: already compressed
+      idx16 = !(flags & RBF_NO_IDX16) && !(flags & RBF_STREAM_LDG);
+    } else if (tf && want16 && N_i >= 4096 && !(flags & RBF_NO_IDX16) && !(flags & RBF_STREAM_LDG) &&
+        !(e && std::atoi(e) == 0)) {
+      RBF_TRY(dev_alloc(p.get(), &p->C16, sell));
+      RBF_TRY(dev_alloc(p.get(), &p->meta, static_cast<size_t>(p->S)));
+      unsigned long long* d_over = nullptr;
+      RBF_TRY(pool_alloc(&d_over, 1, p->stream));
+      RBF_CK(cudaMemsetAsync(d_over, 0, sizeof(unsigned long long), p->stream));
+      const int blocks = static_cast<int>(std::min<int64_t>((p->S * 32 + 255) / 256, 148 * 16));
+      rbf::compress_ids_kernel<<<blocks, 256, 0, p->stream>>>(p->C, N_i, n, p->C16, p->meta, d_over);
+      RBF_CK(cudaGetLastError());
+      unsigned long long over = 0;
+      RBF_CK(cudaMemcpyAsync(&over, d_over, sizeof(over), cudaMemcpyDeviceToHost, p->stream));
+      RBF_CK(cudaStreamSynchronize(p->stream));
+      pool_free(d_over, p->stream);
+      const bool force = e && std::atoi(e) == 2;  // tests: exercise the overflow path
+      if (force || over * 20 <= static_cast<unsigned long long>(p->S)) {  // <= 5 % of the slices overflow
+        idx16 = true;
+        p->overflow_slices = static_cast<int64_t>(over);
+      } else {
+        pool_free(p->C16, p->stream);
+        pool_free(p->meta, p->stream);
+        p->device_bytes -= static_cast<int64_t>(sell * sizeof(unsigned short) + p->S * sizeof(int4));
+      }
+    }
+  }
+  pick_kernels(n, rpl_req, idx16 && rpl_req != 2, &p->stream_fn, &p->resident_fn, &tma_fn, &p->kernel_n,
+               &rpl, &cw);
+  p->index_bits = (idx16 && rpl_req != 2) ? 16 : 32;
+  const int64_t rows_pad = ((N_i + 31) / 32) * 32;
+  const size_t smem = static_cast<size_t>(rows_pad) * n * (sizeof(double) + sizeof(int)) +
+                      static_cast<size_t>(rows_pad) * sizeof(double) +
+                      2 * static_cast<size_t>(N) * sizeof(double);
+  if (!(flags & RBF_NO_RESIDENT) && N_i > 0 && smem <= kResidentSmemMax - 1024) {
+    if (set_max_smem(p->resident_fn) == cudaSuccess) {
+      p->resident = true;
+      p->resident_smem = smem;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  // cluster-resident loop: rows spread over Q SMs of one cluster (DSMEM halo)
+  if (!(flags & RBF_NO_RESIDENT) && !(flags & RBF_NO_CLUSTER) && N_i >= 256) {
+    // 4-8 CTAs measured best on the paper's Fig. 1 case (1.01 / 1.04 us/step vs
+    // 1.30 at 16, profiles/README.md); more when a CTA would own more than 256
+    // rows (register-resident variant) or its rows would not fit
+    const size_t NU = static_cast<size_t>(((B + 1) & ~int64_t(1)) + N_i + 2);
+    auto smem_for = [&](int qq) {
+      const int rpc_ = static_cast<int>(((N_i + qq - 1) / qq + 1) & ~int64_t(1));
+      return 2 * NU * 8 + 2 * 16 * 32 * 2 * 8 + static_cast<size_t>(n) * rpc_ * 12 + rpc_ * 8 + rpc_ * 4;
+    };
+    int q = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(4, (N_i + 255) / 256)));
+    while (q < 16 && smem_for(q) > 200 * 1024) ++q;
+    if (const char* e = std::getenv("RBFFD_CLUSTER")) q = std::max(2, std::min(16, std::atoi(e)));
+    const int rpc = static_cast<int>(((N_i + q - 1) / q + 1) & ~int64_t(1));
+    const size_t csmem = smem_for(q);
+    ClusterFn cfn = nullptr;
+    switch (n) {
+#define RBF_CCASE(K) \
+  case K:            \
+    cfn = KernelSet<K>::cluster(rpc <= 256); \
+    break;
+      RBF_SPECIALISED(RBF_CCASE)
+#undef RBF_CCASE
+      default:
+        cfn = KernelSet<0>::cluster(rpc <= 256);
+    }
+    const int threads = std::min(1024, ((rpc + 31) / 32) * 32);
+    if (csmem <= 200 * 1024 && rpc <= 1024 &&
+        set_max_smem(cfn) == cudaSuccess &&
+        (q <= 8 || cudaFuncSetAttribute(cfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(q);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = csmem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = q;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, cfn, &cfg) == cudaSuccess && nclusters >= 1) {
+        RBF_TRY(dev_alloc(p.get(), &p->cluster_dest, static_cast<size_t>(N_i)));
+        RBF_CK(cudaMemsetAsync(p->cluster_dest, 0, sizeof(unsigned int) * N_i, p->stream));
+        const int blocks = static_cast<int>(std::min<int64_t>((N_i * n + 255) / 256, 148 * 16));
+        rbf::cluster_dest_kernel<<<blocks, 256, 0, p->stream>>>(p->C, N_i, n, B, rpc, p->cluster_dest);
+        RBF_CK(cudaGetLastError());
+        p->cluster_fn = cfn;
+        p->cluster_q = q;
+        p->cluster_rpc = rpc;
+        p->cluster_threads = threads;
+        p->cluster_smem = csmem;
+        p->resident = true;
+      }
+    }
+    cudaGetLastError();
+  }
+  int sms = 148, per_sm = 1;
+  RBF_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  p->variant = p->cluster_fn ? 3 : (p->resident ? 0 : 1);
+  if (tma_fn && !(flags & RBF_STREAM_LDG) && N_i > 0) {
+    // ring geometry: ~24 KB stages, as many as fit in ~200 KB of shared memory
+    const int slice = n * 32 * (8 + p->index_bits / 8) + 32 * 8 + (p->index_bits == 16 ? 16 : 0);
+    int sps = std::max(1, 24576 / slice);
+    if (const char* e = std::getenv("RBFFD_TMA_SPS")) sps = std::max(1, std::atoi(e));
+    sps = std::max(rpl, (sps / rpl) * rpl);
+    const int stage = sps * slice;
+    int stages = std::max(2, std::min(8, static_cast<int>((200 * 1024) / stage)));
+    if (const char* e = std::getenv("RBFFD_TMA_STAGES")) stages = std::max(2, std::min(16, std::atoi(e)));
+    const size_t smem_t = 2 * 16 * sizeof(uint64_t) + static_cast<size_t>(stages) * stage;
+    if (smem_t <= kResidentSmemMax && set_max_smem(tma_fn) == cudaSuccess) {
+      p->tma_fn = tma_fn;
+      p->tma_geom = rbf::TmaGeom{sps, stages, std::getenv("RBFFD_TMA_CONTIG") ? 1 : 0};
+      p->tma_smem = smem_t;
+      p->tma_block = 32 * (cw + 1);
+      const int64_t chunks = (p->S + sps - 1) / sps;
+      int occ = 1;
+      RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tma_fn, p->tma_block, smem_t));
+      p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(chunks, int64_t(sms) * std::max(occ, 1))));
+      if (!p->resident && !p->cluster_fn) p->variant = 2;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  // dataflow loop: one CTA per SM, contiguous slice ranges, neighbour waits
+  const char* flow_env = std::getenv("RBFFD_FLOW");
+  if (p->tma_fn && ((flags & RBF_FLOW) || (flow_env && std::atoi(flow_env) == 1))) {
+    FlowFn ffn = nullptr;
+    switch (n) {
+#define RBF_FCASE(K) \
+  case K:            \
+    ffn = KernelSet<K>::flow(p->index_bits == 16); \
+    break;
+      RBF_SPECIALISED(RBF_FCASE)
+#undef RBF_FCASE
+      default:
+        ffn = nullptr;
+    }
+    int occ = 0;
+    if (ffn && set_max_smem(ffn) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ffn, p->tma_block, p->tma_smem) == cudaSuccess &&
+        occ >= 1) {
+      const int G = sms;  // one CTA per SM (the ring fills the shared memory)
+      const int spc = static_cast<int>((p->S + G - 1) / G);
+      if (p->S >= 4LL * G && spc >= p->tma_geom.sps) {
+        const int words = (G + 31) / 32;
+        unsigned int* d_mat = nullptr;
+        RBF_TRY(pool_alloc(&d_mat, static_cast<size_t>(G) * words, p->stream));
+        RBF_CK(cudaMemsetAsync(d_mat, 0, sizeof(unsigned int) * G * words, p->stream));
+        const int blocks = static_cast<int>(std::min<int64_t>((N_i * n + 255) / 256, 148 * 16));
+        rbf::flow_dep_kernel<<<blocks, 256, 0, p->stream>>>(p->C, N_i, n, B, static_cast<long long>(spc) * 32,
+                                                            words, d_mat);
+        RBF_CK(cudaGetLastError());
+        std::vector<unsigned int> mat(static_cast<size_t>(G) * words);
+        RBF_CK(cudaMemcpyAsync(mat.data(), d_mat, sizeof(unsigned int) * mat.size(), cudaMemcpyDeviceToHost,
+                               p->stream));
+        RBF_CK(cudaStreamSynchronize(p->stream));
+        pool_free(d_mat, p->stream);
+        std::vector<int> off(G + 1, 0), dep;
+        int maxdeg = 0;
+        for (int b = 0; b < G; ++b) {
+          for (int c = 0; c < G; ++c)
+            if (mat[static_cast<size_t>(b) * words + (c >> 5)] & (1u << (c & 31))) dep.push_back(c);
+          off[b + 1] = static_cast<int>(dep.size());
+          maxdeg = std::max(maxdeg, off[b + 1] - off[b]);
+        }
+        if (maxdeg <= 160) {
+          RBF_TRY(dev_alloc(p.get(), &p->flow_dep_off, static_cast<size_t>(G + 1)));
+          RBF_TRY(dev_alloc(p.get(), &p->flow_dep, std::max<size_t>(1, dep.size())));
+          RBF_TRY(dev_alloc(p.get(), &p->flow_flags, static_cast<size_t>(G)));
+          RBF_TRY(dev_alloc(p.get(), &p->u_init, static_cast<size_t>(N)));
+          RBF_CK(cudaMemcpyAsync(p->flow_dep_off, off.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice,
+                                 p->stream));
+          if (!dep.empty())
+            RBF_CK(cudaMemcpyAsync(p->flow_dep, dep.data(), sizeof(int) * dep.size(), cudaMemcpyHostToDevice,
+                                   p->stream));
+          RBF_CK(cudaStreamSynchronize(p->stream));
+          p->flow_fn = ffn;
+          p->flow_grid = G;
+          p->flow_spc = spc;
+        }
+      }
+    }
+    cudaGetLastError();
+  }
+  if (!p->tma_fn) {
+    RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p->stream_fn, kStreamBlock, 0));
+    per_sm = std::max(per_sm, 1);
+    const int64_t need = (N_i + kStreamBlock - 1) / kStreamBlock;
+    p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));
+  }
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  return RBF_OK;
+}
+
 int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int64_t* interior,
                      const int64_t* rows, const double* weights, const double* f_int,
                      const double* positions, int32_t device, uint32_t flags, int32_t degree) {
@@ -861,218 +1086,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
     return fail(RBF_ERR_PARAM, "stencil node id out of range");
   }
 
-  // ---- kernel selection -----------------------------------------------------
-  int cw = 8;         // consumer warps of the TMA ring kernel (per width, KernelSet::kCW)
-  int rpl_req = 1;    // rows per lane of the TMA consumers (RBFFD_TMA_RPL=2: two, n <= 20)
-  if (const char* e = std::getenv("RBFFD_TMA_RPL")) rpl_req = std::atoi(e);
-  TmaFn tma_fn = nullptr;
-  int rpl = 1;
-  // 16-bit two-window ids for the TMA ring (only worth it when almost every
-  // slice fits; the rest fall back to int32 ids read from HBM)
-  bool idx16 = false;
-  {
-    StreamFn sf;
-    ResidentFn rf;
-    TmaFn tf = nullptr;
-    int kn, r1, c1;
-    pick_kernels(n, 1, false, &sf, &rf, &tf, &kn, &r1, &c1);
-    const char* e = std::getenv("RBFFD_IDX16");
-    // wide stencils (n > 32) run consumer-bound: the decode costs more than
-    // the saved bytes (C4: 9.40e9 vs 9.72e9 upd/s, profiles/README.md)
-    const bool want16 = (n <= 32) || (e && std::atoi(e) == 2);
-    if (tf && want16 && N_i >= 4096 && !(flags & RBF_NO_IDX16) && !(flags & RBF_STREAM_LDG) &&
-        !(e && std::atoi(e) == 0)) {
-      RBF_TRY(dev_alloc(p.get(), &p->C16, sell));
-      RBF_TRY(dev_alloc(p.get(), &p->meta, static_cast<size_t>(p->S)));
-      unsigned long long* d_over = nullptr;
-      RBF_TRY(pool_alloc(&d_over, 1, p->stream));
-      RBF_CK(cudaMemsetAsync(d_over, 0, sizeof(unsigned long long), p->stream));
-      const int blocks = static_cast<int>(std::min<int64_t>((p->S * 32 + 255) / 256, 148 * 16));
-      rbf::compress_ids_kernel<<<blocks, 256, 0, p->stream>>>(p->C, N_i, n, p->C16, p->meta, d_over);
-      RBF_CK(cudaGetLastError());
-      unsigned long long over = 0;
-      RBF_CK(cudaMemcpyAsync(&over, d_over, sizeof(over), cudaMemcpyDeviceToHost, p->stream));
-      RBF_CK(cudaStreamSynchronize(p->stream));
-      pool_free(d_over, p->stream);
-      const bool force = e && std::atoi(e) == 2;  // tests: exercise the overflow path
-      if (force || over * 20 <= static_cast<unsigned long long>(p->S)) {  // <= 5 % of the slices overflow
-        idx16 = true;
-        p->overflow_slices = static_cast<int64_t>(over);
-      } else {
-        pool_free(p->C16, p->stream);
-        pool_free(p->meta, p->stream);
-        p->device_bytes -= static_cast<int64_t>(sell * sizeof(unsigned short) + p->S * sizeof(int4));
-      }
-    }
-  }
-  pick_kernels(n, rpl_req, idx16 && rpl_req != 2, &p->stream_fn, &p->resident_fn, &tma_fn, &p->kernel_n,
-               &rpl, &cw);
-  p->index_bits = (idx16 && rpl_req != 2) ? 16 : 32;
-  const int64_t rows_pad = ((N_i + 31) / 32) * 32;
-  const size_t smem = static_cast<size_t>(rows_pad) * n * (sizeof(double) + sizeof(int)) +
-                      static_cast<size_t>(rows_pad) * sizeof(double) +
-                      2 * static_cast<size_t>(N) * sizeof(double);
-  if (!(flags & RBF_NO_RESIDENT) && N_i > 0 && smem <= kResidentSmemMax - 1024) {
-    if (set_max_smem(p->resident_fn) == cudaSuccess) {
-      p->resident = true;
-      p->resident_smem = smem;
-    } else {
-      cudaGetLastError();
-    }
-  }
-  // cluster-resident loop: rows spread over Q SMs of one cluster (DSMEM halo)
-  if (!(flags & RBF_NO_RESIDENT) && !(flags & RBF_NO_CLUSTER) && N_i >= 256) {
-    // 4-8 CTAs measured best on the paper's Fig. 1 case (1.01 / 1.04 us/step vs
-    // 1.30 at 16, profiles/README.md); more when a CTA would own more than 256
-    // rows (register-resident variant) or its rows would not fit
-    const size_t NU = static_cast<size_t>(((B + 1) & ~int64_t(1)) + N_i + 2);
-    auto smem_for = [&](int qq) {
-      const int rpc_ = static_cast<int>(((N_i + qq - 1) / qq + 1) & ~int64_t(1));
-      return 2 * NU * 8 + 2 * 16 * 32 * 2 * 8 + static_cast<size_t>(n) * rpc_ * 12 + rpc_ * 8 + rpc_ * 4;
-    };
-    int q = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(4, (N_i + 255) / 256)));
-    while (q < 16 && smem_for(q) > 200 * 1024) ++q;
-    if (const char* e = std::getenv("RBFFD_CLUSTER")) q = std::max(2, std::min(16, std::atoi(e)));
-    const int rpc = static_cast<int>(((N_i + q - 1) / q + 1) & ~int64_t(1));
-    const size_t csmem = smem_for(q);
-    ClusterFn cfn = nullptr;
-    switch (n) {
-#define RBF_CCASE(K) \
-  case K:            \
-    cfn = KernelSet<K>::cluster(rpc <= 256); \
-    break;
-      RBF_SPECIALISED(RBF_CCASE)
-#undef RBF_CCASE
-      default:
-        cfn = KernelSet<0>::cluster(rpc <= 256);
-    }
-    const int threads = std::min(1024, ((rpc + 31) / 32) * 32);
-    if (csmem <= 200 * 1024 && rpc <= 1024 &&
-        set_max_smem(cfn) == cudaSuccess &&
-        (q <= 8 || cudaFuncSetAttribute(cfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(q);
-      cfg.blockDim = dim3(threads);
-      cfg.dynamicSmemBytes = csmem;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = q;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      int nclusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&nclusters, cfn, &cfg) == cudaSuccess && nclusters >= 1) {
-        RBF_TRY(dev_alloc(p.get(), &p->cluster_dest, static_cast<size_t>(N_i)));
-        RBF_CK(cudaMemsetAsync(p->cluster_dest, 0, sizeof(unsigned int) * N_i, p->stream));
-        const int blocks = static_cast<int>(std::min<int64_t>((N_i * n + 255) / 256, 148 * 16));
-        rbf::cluster_dest_kernel<<<blocks, 256, 0, p->stream>>>(p->C, N_i, n, B, rpc, p->cluster_dest);
-        RBF_CK(cudaGetLastError());
-        p->cluster_fn = cfn;
-        p->cluster_q = q;
-        p->cluster_rpc = rpc;
-        p->cluster_threads = threads;
-        p->cluster_smem = csmem;
-        p->resident = true;
-      }
-    }
-    cudaGetLastError();
-  }
-  int sms = 148, per_sm = 1;
-  RBF_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  p->variant = p->cluster_fn ? 3 : (p->resident ? 0 : 1);
-  if (tma_fn && !(flags & RBF_STREAM_LDG) && N_i > 0) {
-    // ring geometry: ~24 KB stages, as many as fit in ~200 KB of shared memory
-    const int slice = n * 32 * (8 + p->index_bits / 8) + 32 * 8 + (p->index_bits == 16 ? 16 : 0);
-    int sps = std::max(1, 24576 / slice);
-    if (const char* e = std::getenv("RBFFD_TMA_SPS")) sps = std::max(1, std::atoi(e));
-    sps = std::max(rpl, (sps / rpl) * rpl);
-    const int stage = sps * slice;
-    int stages = std::max(2, std::min(8, static_cast<int>((200 * 1024) / stage)));
-    if (const char* e = std::getenv("RBFFD_TMA_STAGES")) stages = std::max(2, std::min(16, std::atoi(e)));
-    const size_t smem_t = 2 * 16 * sizeof(uint64_t) + static_cast<size_t>(stages) * stage;
-    if (smem_t <= kResidentSmemMax && set_max_smem(tma_fn) == cudaSuccess) {
-      p->tma_fn = tma_fn;
-      p->tma_geom = rbf::TmaGeom{sps, stages, std::getenv("RBFFD_TMA_CONTIG") ? 1 : 0};
-      p->tma_smem = smem_t;
-      p->tma_block = 32 * (cw + 1);
-      const int64_t chunks = (p->S + sps - 1) / sps;
-      int occ = 1;
-      RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tma_fn, p->tma_block, smem_t));
-      p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(chunks, int64_t(sms) * std::max(occ, 1))));
-      if (!p->resident && !p->cluster_fn) p->variant = 2;
-    } else {
-      cudaGetLastError();
-    }
-  }
-  // dataflow loop: one CTA per SM, contiguous slice ranges, neighbour waits
-  const char* flow_env = std::getenv("RBFFD_FLOW");
-  if (p->tma_fn && ((flags & RBF_FLOW) || (flow_env && std::atoi(flow_env) == 1))) {
-    FlowFn ffn = nullptr;
-    switch (n) {
-#define RBF_FCASE(K) \
-  case K:            \
-    ffn = KernelSet<K>::flow(p->index_bits == 16); \
-    break;
-      RBF_SPECIALISED(RBF_FCASE)
-#undef RBF_FCASE
-      default:
-        ffn = nullptr;
-    }
-    int occ = 0;
-    if (ffn && set_max_smem(ffn) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ffn, p->tma_block, p->tma_smem) == cudaSuccess &&
-        occ >= 1) {
-      const int G = sms;  // one CTA per SM (the ring fills the shared memory)
-      const int spc = static_cast<int>((p->S + G - 1) / G);
-      if (p->S >= 4LL * G && spc >= p->tma_geom.sps) {
-        const int words = (G + 31) / 32;
-        unsigned int* d_mat = nullptr;
-        RBF_TRY(pool_alloc(&d_mat, static_cast<size_t>(G) * words, p->stream));
-        RBF_CK(cudaMemsetAsync(d_mat, 0, sizeof(unsigned int) * G * words, p->stream));
-        const int blocks = static_cast<int>(std::min<int64_t>((N_i * n + 255) / 256, 148 * 16));
-        rbf::flow_dep_kernel<<<blocks, 256, 0, p->stream>>>(p->C, N_i, n, B, static_cast<long long>(spc) * 32,
-                                                            words, d_mat);
-        RBF_CK(cudaGetLastError());
-        std::vector<unsigned int> mat(static_cast<size_t>(G) * words);
-        RBF_CK(cudaMemcpyAsync(mat.data(), d_mat, sizeof(unsigned int) * mat.size(), cudaMemcpyDeviceToHost,
-                               p->stream));
-        RBF_CK(cudaStreamSynchronize(p->stream));
-        pool_free(d_mat, p->stream);
-        std::vector<int> off(G + 1, 0), dep;
-        int maxdeg = 0;
-        for (int b = 0; b < G; ++b) {
-          for (int c = 0; c < G; ++c)
-            if (mat[static_cast<size_t>(b) * words + (c >> 5)] & (1u << (c & 31))) dep.push_back(c);
-          off[b + 1] = static_cast<int>(dep.size());
-          maxdeg = std::max(maxdeg, off[b + 1] - off[b]);
-        }
-        if (maxdeg <= 160) {
-          RBF_TRY(dev_alloc(p.get(), &p->flow_dep_off, static_cast<size_t>(G + 1)));
-          RBF_TRY(dev_alloc(p.get(), &p->flow_dep, std::max<size_t>(1, dep.size())));
-          RBF_TRY(dev_alloc(p.get(), &p->flow_flags, static_cast<size_t>(G)));
-          RBF_TRY(dev_alloc(p.get(), &p->u_init, static_cast<size_t>(N)));
-          RBF_CK(cudaMemcpyAsync(p->flow_dep_off, off.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice,
-                                 p->stream));
-          if (!dep.empty())
-            RBF_CK(cudaMemcpyAsync(p->flow_dep, dep.data(), sizeof(int) * dep.size(), cudaMemcpyHostToDevice,
-                                   p->stream));
-          RBF_CK(cudaStreamSynchronize(p->stream));
-          p->flow_fn = ffn;
-          p->flow_grid = G;
-          p->flow_spc = spc;
-        }
-      }
-    }
-    cudaGetLastError();
-  }
-  if (!p->tma_fn) {
-    RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p->stream_fn, kStreamBlock, 0));
-    per_sm = std::max(per_sm, 1);
-    const int64_t need = (N_i + kStreamBlock - 1) / kStreamBlock;
-    p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * per_sm)));
-  }
-  RBF_CK(cudaStreamSynchronize(p->stream));
+  RBF_TRY(finish_plan(p, flags));
   timer.mark("kernel selection");
   *out = p.release();
   return RBF_OK;
@@ -1175,6 +1189,141 @@ int rbf_plan_weight_row_sum_max(rbf_plan* p, double* out) {
   RBF_CK(cudaMemcpyAsync(out, d, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
   RBF_CK(cudaStreamSynchronize(p->stream));
   pool_free(d, p->stream);
+  return RBF_OK;
+}
+
+// ---- plan files: the packed device layout on disk ------
+struct PlanFileHeader {
+  char magic[8];  // "RBFPLAN1"
+  int32_t version, n;
+  int64_t N, N_i, B, S;
+  int32_t index_bits, renumbered;
+  int64_t overflow_slices;
+  int64_t reserved[4];
+};
+
+static int file_io(std::FILE* f, void* dev, size_t bytes, bool save, cudaStream_t stream) {
+  Staging& sg = staging();
+  std::lock_guard<std::mutex> lock(sg.mu);
+  int dev_id = 0;
+  cudaGetDevice(&dev_id);
+  RBF_TRY(staging_acquire(sg, dev_id));
+  unsigned char* d = static_cast<unsigned char*>(dev);
+  for (size_t off = 0; off < bytes; off += sg.cap) {
+    const size_t len = std::min(sg.cap, bytes - off);
+    if (save) {
+      RBF_CK(cudaMemcpyAsync(sg.buf[0], d + off, len, cudaMemcpyDeviceToHost, stream));
+      RBF_CK(cudaStreamSynchronize(stream));
+      if (std::fwrite(sg.buf[0], 1, len, f) != len) return fail(RBF_ERR_PARAM, "plan file: write failed");
+    } else {
+      if (std::fread(sg.buf[0], 1, len, f) != len) return fail(RBF_ERR_PARAM, "plan file: truncated");
+      RBF_CK(cudaMemcpyAsync(d + off, sg.buf[0], len, cudaMemcpyHostToDevice, stream));
+      RBF_CK(cudaStreamSynchronize(stream));
+    }
+  }
+  return RBF_OK;
+}
+
+int rbf_plan_save(const rbf_plan* cp, const char* path) {
+  if (!cp || !path) return fail(RBF_ERR_PARAM, "NULL argument");
+  rbf_plan* p = const_cast<rbf_plan*>(cp);
+  RBF_CK(cudaSetDevice(p->device));
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(RBF_ERR_PARAM, std::string("cannot open ") + path);
+  PlanFileHeader h = {};
+  std::memcpy(h.magic, "RBFPLAN1", 8);
+  h.version = 1;
+  h.n = p->n;
+  h.N = p->N;
+  h.N_i = p->N_i;
+  h.B = p->B;
+  h.S = p->S;
+  h.index_bits = p->C16 ? 16 : 32;
+  h.renumbered = p->renumbered ? 1 : 0;
+  h.overflow_slices = p->overflow_slices;
+  int rc = std::fwrite(&h, sizeof(h), 1, f) == 1 ? RBF_OK : fail(RBF_ERR_PARAM, "plan file: write failed");
+  const size_t sell = static_cast<size_t>(p->S) * 32 * p->n;
+  if (rc == RBF_OK) rc = file_io(f, p->W, sell * sizeof(double), true, p->stream);
+  if (rc == RBF_OK) rc = file_io(f, p->C, sell * sizeof(int), true, p->stream);
+  if (rc == RBF_OK) rc = file_io(f, p->F, static_cast<size_t>(p->S) * 32 * sizeof(double), true, p->stream);
+  if (rc == RBF_OK && p->C16) {
+    rc = file_io(f, p->C16, sell * sizeof(unsigned short), true, p->stream);
+    if (rc == RBF_OK) rc = file_io(f, p->meta, static_cast<size_t>(p->S) * sizeof(int4), true, p->stream);
+  }
+  if (rc == RBF_OK && p->renumbered) {
+    rc = file_io(f, p->new_id, static_cast<size_t>(p->N) * sizeof(int), true, p->stream);
+    if (rc == RBF_OK) rc = file_io(f, p->row_of_k, static_cast<size_t>(p->N_i) * sizeof(long long), true, p->stream);
+  }
+  if (std::fclose(f) != 0 && rc == RBF_OK) rc = fail(RBF_ERR_PARAM, "plan file: close failed");
+  return rc;
+}
+
+int rbf_plan_load(rbf_plan** out, const char* path, int32_t device, uint32_t flags) {
+  if (!out || !path) return fail(RBF_ERR_PARAM, "NULL argument");
+  *out = nullptr;
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) return fail(RBF_ERR_PARAM, std::string("cannot open ") + path);
+  PlanFileHeader h = {};
+  if (std::fread(&h, sizeof(h), 1, f) != 1 || std::memcmp(h.magic, "RBFPLAN1", 8) != 0 || h.version != 1 ||
+      h.n < 1 || h.N < 1 || h.N_i < 0 || h.N_i > h.N || h.S != (h.N_i + 31) / 32 || h.B != h.N - h.N_i) {
+    std::fclose(f);
+    return fail(RBF_ERR_PARAM, "not an rbffd_b200 plan file (or a different version)");
+  }
+  std::unique_ptr<rbf_plan> p(new rbf_plan());
+  p->device = device;
+  p->N = h.N;
+  p->N_i = h.N_i;
+  p->B = h.B;
+  p->n = h.n;
+  p->S = h.S;
+  p->renumbered = h.renumbered != 0;
+  p->pdl = (flags & RBF_NO_PDL) == 0;
+  p->overflow_slices = h.overflow_slices;
+  int rc = RBF_OK;
+  auto step = [&](int r) { if (rc == RBF_OK) rc = r; };
+  step(cudaSetDevice(device) == cudaSuccess ? RBF_OK : fail(RBF_ERR_CUDA, "cudaSetDevice"));
+  step(prepare_pool(device));
+  if (rc == RBF_OK) {
+    step(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) == cudaSuccess ? RBF_OK : fail(RBF_ERR_CUDA, "stream"));
+    step(cudaEventCreate(&p->ev0) == cudaSuccess ? RBF_OK : fail(RBF_ERR_CUDA, "event"));
+    step(cudaEventCreate(&p->ev1) == cudaSuccess ? RBF_OK : fail(RBF_ERR_CUDA, "event"));
+    step(cudaMallocHost(reinterpret_cast<void**>(&p->h_st), sizeof(rbf::DevStatus)) == cudaSuccess
+             ? RBF_OK : fail(RBF_ERR_CUDA, "host status"));
+  }
+  const size_t sell = static_cast<size_t>(p->S) * 32 * p->n;
+  if (rc == RBF_OK) step(dev_alloc(p.get(), &p->st, 1));
+  if (rc == RBF_OK) step(dev_alloc(p.get(), &p->W, sell));
+  if (rc == RBF_OK) step(dev_alloc(p.get(), &p->C, sell));
+  if (rc == RBF_OK) step(dev_alloc(p.get(), &p->F, static_cast<size_t>(p->S) * 32));
+  if (rc == RBF_OK) step(dev_alloc(p.get(), &p->U[0], static_cast<size_t>(p->N)));
+  if (rc == RBF_OK) step(dev_alloc(p.get(), &p->U[1], static_cast<size_t>(p->N)));
+  if (rc == RBF_OK) step(file_io(f, p->W, sell * sizeof(double), false, p->stream));
+  if (rc == RBF_OK) step(file_io(f, p->C, sell * sizeof(int), false, p->stream));
+  if (rc == RBF_OK) step(file_io(f, p->F, static_cast<size_t>(p->S) * 32 * sizeof(double), false, p->stream));
+  if (rc == RBF_OK && h.index_bits == 16) {
+    step(dev_alloc(p.get(), &p->C16, sell));
+    step(dev_alloc(p.get(), &p->meta, static_cast<size_t>(p->S)));
+    step(file_io(f, p->C16, sell * sizeof(unsigned short), false, p->stream));
+    step(file_io(f, p->meta, static_cast<size_t>(p->S) * sizeof(int4), false, p->stream));
+  }
+  if (rc == RBF_OK && p->renumbered) {
+    step(dev_alloc(p.get(), &p->new_id, static_cast<size_t>(p->N)));
+    step(dev_alloc(p.get(), &p->tmp, static_cast<size_t>(p->N)));
+    step(dev_alloc(p.get(), &p->row_of_k, static_cast<size_t>(std::max<int64_t>(1, p->N_i))));
+    step(file_io(f, p->new_id, static_cast<size_t>(p->N) * sizeof(int), false, p->stream));
+    step(file_io(f, p->row_of_k, static_cast<size_t>(p->N_i) * sizeof(long long), false, p->stream));
+  }
+  std::fclose(f);
+  if (rc == RBF_OK) {
+    RBF_CK(cudaMemsetAsync(p->U[0], 0, sizeof(double) * p->N, p->stream));
+    RBF_CK(cudaMemsetAsync(p->U[1], 0, sizeof(double) * p->N, p->stream));
+    step(finish_plan(p, flags));
+  }
+  if (rc != RBF_OK) {
+    rbf_plan_destroy(p.release());
+    return rc;
+  }
+  *out = p.release();
   return RBF_OK;
 }
 

@@ -138,3 +138,44 @@ def load_fixture(path) -> tuple[NodeSet, StencilSet, ShapeStore]:
         stencils=stencils,
     )
     return nodes, stencils, shapes
+
+
+def save_problem(path, nodes: NodeSet, stencils: StencilSet, shapes: ShapeStore) -> None:
+    """Binary problem cache: one .npy per array in a
+    directory, replacing the reference's 17-digit CSV files for large runs
+    (geometry.py:201-220, neighborhoods.py:104-122, weights.py:209-215).
+    Node ids are stored as int32 when N < 2^31 (half the reference's int64)."""
+    import json
+    from pathlib import Path
+
+    d = Path(path)
+    d.mkdir(parents=True, exist_ok=True)
+    idt = np.int32 if nodes.n_total < 2**31 else np.int64
+    np.save(d / "positions.npy", np.ascontiguousarray(nodes.positions, dtype=np.float64))
+    np.save(d / "is_boundary.npy", np.ascontiguousarray(nodes.is_boundary, dtype=bool))
+    np.save(d / "neighbors.npy", np.ascontiguousarray(stencils.neighbors, dtype=idt))
+    np.save(d / "interior.npy", np.ascontiguousarray(shapes.interior_nodes, dtype=idt))
+    np.save(d / "weights.npy", np.ascontiguousarray(shapes.weights, dtype=np.float64))
+    (d / "meta.json").write_text(json.dumps({"h": float(nodes.h), "n": int(stencils.n),
+                                             "degree": int(shapes.degree), "version": 1}))
+
+
+def load_problem(path, mmap: bool = True):
+    """(nodes, stencils, shapes) from ``save_problem``; the large arrays are
+    memory-mapped (read lazily, straight from the page cache)."""
+    import json
+    from pathlib import Path
+
+    d = Path(path)
+    meta = json.loads((d / "meta.json").read_text())
+    mode = "r" if mmap else None
+    positions = np.load(d / "positions.npy", mmap_mode=mode)
+    is_boundary = np.load(d / "is_boundary.npy")
+    neighbors = np.load(d / "neighbors.npy", mmap_mode=mode)
+    interior = np.load(d / "interior.npy").astype(np.int64)
+    weights = np.load(d / "weights.npy", mmap_mode=mode)
+    nodes = NodeSet(positions=positions, is_boundary=is_boundary, h=float(meta["h"]))
+    stencils = StencilSet(n=int(meta["n"]), neighbors=neighbors)
+    shapes = ShapeStore(degree=int(meta["degree"]), interior_nodes=interior, weights=weights,
+                        stencils=stencils)
+    return nodes, stencils, shapes

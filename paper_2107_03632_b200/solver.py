@@ -223,6 +223,29 @@ class Plan:
         self._finalizer = weakref.finalize(self, self._lib.rbf_plan_destroy, handle)
         return self
 
+    def save(self, path) -> None:
+        """Write the packed device layout to `path` (rbf_plan_save)."""
+        self._check(self._lib.rbf_plan_save(self._h, str(path).encode()))
+
+    @classmethod
+    def load(cls, path, *, device: int = 0, resident: bool = True, pdl: bool = True,
+             tma: bool = True, cluster: bool = True, idx16: bool = True) -> "Plan":
+        """Load a plan written by ``save`` straight into HBM (rbf_plan_load)."""
+        import numpy as _np  # noqa: F401
+
+        self = cls.__new__(cls)
+        self._lib = _lib.load()
+        flags = (0 if resident else _lib.RBF_NO_RESIDENT) | (0 if pdl else _lib.RBF_NO_PDL) \
+            | (0 if tma else _lib.RBF_STREAM_LDG) | (0 if cluster else _lib.RBF_NO_CLUSTER) \
+            | (0 if idx16 else _lib.RBF_NO_IDX16)
+        handle = ctypes.c_void_p()
+        self._check(self._lib.rbf_plan_load(ctypes.byref(handle), str(path).encode(), int(device), flags))
+        self._h = handle
+        self._finalizer = weakref.finalize(self, self._lib.rbf_plan_destroy, handle)
+        info = self.info()
+        self.n_total, self.n_rows, self.n = int(info["N"]), int(info["N_i"]), int(info["n"])
+        return self
+
     def weight_row_sum_max(self) -> float:
         """max_k sum_j |w_kj| on the device (stability_bound = 2 / this)."""
         out = ctypes.c_double()

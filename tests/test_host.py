@@ -122,3 +122,18 @@ def test_solution_csv_and_report_json(tmp_path, golden):
     loaded = json.loads(jpath.read_text())
     assert set(loaded) == {"steps", "wall_time_s", "linf", "l2", "residual", "config"}
     assert loaded["steps"] == 50 and loaded["config"]["m"] == 2
+
+
+def test_problem_cache_round_trip(tmp_path, golden):
+    """Binary problem cache (save_problem / load_problem, memory-mapped)."""
+    nodes, stencils, shapes, _ = golden("m4")
+    rb.save_problem(tmp_path / "p", nodes, stencils, shapes)
+    n2, s2, sh2 = rb.load_problem(tmp_path / "p")
+    assert np.array_equal(n2.positions, nodes.positions)
+    assert np.array_equal(n2.is_boundary, nodes.is_boundary) and n2.h == nodes.h
+    assert np.array_equal(s2.neighbors, stencils.neighbors) and s2.n == stencils.n
+    assert np.array_equal(sh2.interior_nodes, shapes.interior_nodes)
+    assert np.array_equal(sh2.weights, shapes.weights) and sh2.degree == shapes.degree
+    # host prep is unchanged on memory-mapped arrays
+    assert rb.stability_bound(sh2) == rb.stability_bound(shapes)
+    assert np.array_equal(rb.forcing(n2.positions), rb.forcing(nodes.positions))

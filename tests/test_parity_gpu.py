@@ -554,3 +554,41 @@ def test_streaming_variants_on_tiny_row_counts(n_rows):
         assert np.array_equal(plan.get_field(), want), kw
         plan.close()
     del u2
+
+
+
+@pytest.mark.parametrize("which", ["dome", "crit6", "synthetic"])
+def test_plan_file_round_trip_is_bitwise(golden, synth_cache, tmp_path, which):
+    """rbf_plan_save / rbf_plan_load: the loaded plan (no packing, renumbering
+    or id compression at load) runs bit-identically to the saved one."""
+    if which == "synthetic":
+        nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
+    else:
+        nodes, _, shapes, _ = golden(which)
+    interior = shapes.interior_nodes
+    plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                rb.forcing(nodes.positions[interior]), nodes.positions, renumber=True)
+    path = tmp_path / "plan.rbf"
+    plan.save(path)
+    loaded = Plan.load(path)
+    a, b = plan.info(), loaded.info()
+    for k in ("N", "N_i", "n", "variant", "index_bits", "renumbered"):
+        assert a[k] == b[k], k
+    u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    dt = 0.5 * rb.stability_bound(shapes)
+    out = []
+    for p in (plan, loaded):
+        p.set_field(u0)
+        r = p.run(dt, steps=130)
+        out.append((p.get_field(), r.residual))
+    assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
+    want = orc.run_time_loop(nodes, shapes, steps=130)
+    assert np.array_equal(out[1][0], want["field"])
+    bad = tmp_path / "bad.rbf"
+    bad.write_bytes(b"not a plan" * 10)
+    with pytest.raises(rb.ParameterError):
+        Plan.load(bad)
+    trunc = tmp_path / "trunc.rbf"
+    trunc.write_bytes(path.read_bytes()[:200])
+    with pytest.raises(rb.ParameterError):
+        Plan.load(trunc)
