@@ -1202,6 +1202,9 @@ struct PlanFileHeader {
   int64_t reserved[4];
 };
 
+// Device <-> file through the two pinned staging buffers: the disk read of
+// chunk k+1 overlaps the H2D copy of chunk k (load), the D2H copy of chunk k+1
+// overlaps the write of chunk k (save).
 static int file_io(std::FILE* f, void* dev, size_t bytes, bool save, cudaStream_t stream) {
   Staging& sg = staging();
   std::lock_guard<std::mutex> lock(sg.mu);
@@ -1209,18 +1212,36 @@ static int file_io(std::FILE* f, void* dev, size_t bytes, bool save, cudaStream_
   cudaGetDevice(&dev_id);
   RBF_TRY(staging_acquire(sg, dev_id));
   unsigned char* d = static_cast<unsigned char*>(dev);
-  for (size_t off = 0; off < bytes; off += sg.cap) {
-    const size_t len = std::min(sg.cap, bytes - off);
-    if (save) {
-      RBF_CK(cudaMemcpyAsync(sg.buf[0], d + off, len, cudaMemcpyDeviceToHost, stream));
-      RBF_CK(cudaStreamSynchronize(stream));
-      if (std::fwrite(sg.buf[0], 1, len, f) != len) return fail(RBF_ERR_PARAM, "plan file: write failed");
-    } else {
-      if (std::fread(sg.buf[0], 1, len, f) != len) return fail(RBF_ERR_PARAM, "plan file: truncated");
-      RBF_CK(cudaMemcpyAsync(d + off, sg.buf[0], len, cudaMemcpyHostToDevice, stream));
-      RBF_CK(cudaStreamSynchronize(stream));
+  const size_t nchunks = (bytes + sg.cap - 1) / sg.cap;
+  auto len_of = [&](size_t c) { return std::min(sg.cap, bytes - c * sg.cap); };
+  if (save) {
+    if (nchunks) {
+      RBF_CK(cudaMemcpyAsync(sg.buf[0], d, len_of(0), cudaMemcpyDeviceToHost, stream));
+      RBF_CK(cudaEventRecord(sg.ev[0], stream));
     }
+    for (size_t c = 0; c < nchunks; ++c) {
+      const int b = static_cast<int>(c & 1);
+      if (c + 1 < nchunks) {  // start the next D2H into the other buffer
+        RBF_CK(cudaMemcpyAsync(sg.buf[b ^ 1], d + (c + 1) * sg.cap, len_of(c + 1), cudaMemcpyDeviceToHost, stream));
+        RBF_CK(cudaEventRecord(sg.ev[b ^ 1], stream));
+      }
+      RBF_CK(cudaEventSynchronize(sg.ev[b]));
+      if (std::fwrite(sg.buf[b], 1, len_of(c), f) != len_of(c)) return fail(RBF_ERR_PARAM, "plan file: write failed");
+    }
+    RBF_CK(cudaStreamSynchronize(stream));
+    return RBF_OK;
   }
+  for (size_t c = 0; c < nchunks; ++c) {
+    const int b = static_cast<int>(c & 1);
+    RBF_CK(cudaEventSynchronize(sg.ev[b]));  // the H2D out of this buffer (chunk c-2) is done
+    if (std::fread(sg.buf[b], 1, len_of(c), f) != len_of(c)) {
+      cudaStreamSynchronize(stream);
+      return fail(RBF_ERR_PARAM, "plan file: truncated");
+    }
+    RBF_CK(cudaMemcpyAsync(d + c * sg.cap, sg.buf[b], len_of(c), cudaMemcpyHostToDevice, stream));
+    RBF_CK(cudaEventRecord(sg.ev[b], stream));
+  }
+  RBF_CK(cudaStreamSynchronize(stream));
   return RBF_OK;
 }
 
