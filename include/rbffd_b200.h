@@ -99,6 +99,15 @@ int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows
                          int32_t n, int32_t degree, double* weights_out, int64_t* bad_row,
                          int32_t device);
 
+/*
+ * Exact k-nearest-neighbour supports on the device (
+ * rbffd.neighborhoods.build_stencils, neighborhoods.py:51-94): row i of
+ * neighbors_out[N*n] lists the n nodes nearest to node i sorted by
+ * (distance, index) with distance = sqrt(dx*dx + dy*dy) in IEEE double --
+ * the reference's tie rule (tests/oracles.py:16-24).  1 <= n <= min(N, 128).
+ */
+int rbf_knn(const double* positions, int64_t N, int32_t n, int64_t* neighbors_out, int32_t device);
+
 /* rbf_plan_create with the weights assembled on the device straight into the
  * SELL layout (the host never holds them; positions are required). */
 int rbf_plan_create_assembled(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, int32_t degree,

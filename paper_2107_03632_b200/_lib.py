@@ -55,6 +55,7 @@ EXPORTED = (
     "rbf_plan_weight_row_sum_max",
     "rbf_plan_save",
     "rbf_plan_load",
+    "rbf_knn",
 )
 
 
@@ -142,6 +143,7 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "rbf_plan_weight_row_sum_max": ([vp, pdbl], i32),
         "rbf_plan_save": ([vp, ctypes.c_char_p], i32),
         "rbf_plan_load": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, u32], i32),
+        "rbf_knn": ([vp, i64, i32, vp, i32], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

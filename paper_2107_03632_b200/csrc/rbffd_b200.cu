@@ -18,6 +18,9 @@
 #include "step_kernels.cuh"
 #include "weights_kernels.cuh"
 #include "flow_kernels.cuh"
+#include "knn_kernels.cuh"
+
+#include <cub/cub.cuh>
 
 #include <cuda_runtime.h>
 
@@ -1173,6 +1176,92 @@ int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows
     return fail(RBF_ERR_PARAM, "degenerate stencil at interior row " + std::to_string(bad));
   }
   return RBF_OK;
+}
+
+int rbf_knn(const double* positions, int64_t N, int32_t n, int64_t* neighbors_out, int32_t device) {
+  if (!positions || !neighbors_out) return fail(RBF_ERR_PARAM, "NULL argument");
+  if (N < 1 || N > std::numeric_limits<int32_t>::max()) return fail(RBF_ERR_PARAM, "N must be in [1, 2^31-1]");
+  if (n < 1 || n > N) return fail(RBF_ERR_PARAM, "support size n=" + std::to_string(n) + " outside [1, N]");
+  if (n > 128) return fail(RBF_ERR_PARAM, "support size above 128 is not supported on the GPU path");
+  double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
+  for (int64_t i = 0; i < N; ++i) {
+    const double x = positions[2 * i], y = positions[2 * i + 1];
+    if (!std::isfinite(x) || !std::isfinite(y)) return fail(RBF_ERR_PARAM, "non-finite node position");
+    xmin = std::min(xmin, x);
+    xmax = std::max(xmax, x);
+    ymin = std::min(ymin, y);
+    ymax = std::max(ymax, y);
+  }
+  rbf::KnnGrid g;
+  const double w = std::max(xmax - xmin, 1e-300), h = std::max(ymax - ymin, 1e-300);
+  double c = std::sqrt(2.0 * w * h / static_cast<double>(N));  // ~2 points per cell
+  if (!(c > 0)) c = std::max(w, h);
+  c = std::max(c, std::max(w, h) / 32768.0);
+  g.c = c;
+  g.inv_c = 1.0 / c;
+  g.x0 = xmin;
+  g.y0 = ymin;
+  g.nx = static_cast<int>(w / c) + 1;
+  g.ny = static_cast<int>(h / c) + 1;
+  const int64_t cells = static_cast<int64_t>(g.nx) * g.ny;
+  RBF_CK(cudaSetDevice(device));
+  RBF_TRY(prepare_pool(device));
+  cudaStream_t st;
+  RBF_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  double* d_pos = nullptr;
+  int* d_cell = nullptr;
+  int* d_sorted = nullptr;
+  unsigned int* d_count = nullptr;
+  unsigned int* d_start = nullptr;
+  long long* d_out = nullptr;
+  void* d_tmp = nullptr;
+  size_t tmp_bytes = 0;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(N, (int64_t(1) << 25) / n));
+  int rc = RBF_OK;
+  auto ck = [&](cudaError_t e, const char* what) {
+    if (rc == RBF_OK && e != cudaSuccess) rc = fail(RBF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  };
+  ck(cudaMallocAsync(&d_pos, sizeof(double) * 2 * N, st), "alloc");
+  ck(cudaMallocAsync(&d_cell, sizeof(int) * N, st), "alloc");
+  ck(cudaMallocAsync(&d_sorted, sizeof(int) * N, st), "alloc");
+  ck(cudaMallocAsync(&d_count, sizeof(unsigned int) * (cells + 1), st), "alloc");
+  ck(cudaMallocAsync(&d_start, sizeof(unsigned int) * (cells + 1), st), "alloc");
+  ck(cudaMallocAsync(&d_out, sizeof(long long) * chunk * n, st), "alloc");
+  ck(cudaMemcpyAsync(d_pos, positions, sizeof(double) * 2 * N, cudaMemcpyHostToDevice, st), "upload");
+  ck(cudaMemsetAsync(d_count, 0, sizeof(unsigned int) * (cells + 1), st), "memset");
+  const int blocks = static_cast<int>(std::min<int64_t>((N + 255) / 256, 148 * 16));
+  if (rc == RBF_OK) {
+    rbf::knn_count_kernel<<<blocks, 256, 0, st>>>(d_pos, N, g, d_cell, d_count);
+    ck(cudaGetLastError(), "count");
+    ck(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_count, d_start, static_cast<int>(cells + 1), st), "scan");
+    ck(cudaMallocAsync(&d_tmp, std::max<size_t>(tmp_bytes, 16), st), "alloc");
+    ck(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_count, d_start, static_cast<int>(cells + 1), st), "scan");
+    ck(cudaMemcpyAsync(d_count, d_start, sizeof(unsigned int) * (cells + 1), cudaMemcpyDeviceToDevice, st), "copy");
+    rbf::knn_fill_kernel<<<blocks, 256, 0, st>>>(d_cell, N, d_count, d_sorted);
+    ck(cudaGetLastError(), "fill");
+  }
+  for (int64_t q0 = 0; q0 < N && rc == RBF_OK; q0 += chunk) {
+    const int64_t nq = std::min<int64_t>(chunk, N - q0);
+    const int qb = static_cast<int>(std::min<int64_t>((nq + 127) / 128, 148 * 32));
+    if (n <= 16) rbf::knn_query_kernel<16><<<qb, 128, 0, st>>>(d_pos, N, g, d_start, d_sorted, n, q0, nq, d_out);
+    else if (n <= 32) rbf::knn_query_kernel<32><<<qb, 128, 0, st>>>(d_pos, N, g, d_start, d_sorted, n, q0, nq, d_out);
+    else if (n <= 64) rbf::knn_query_kernel<64><<<qb, 128, 0, st>>>(d_pos, N, g, d_start, d_sorted, n, q0, nq, d_out);
+    else rbf::knn_query_kernel<128><<<qb, 128, 0, st>>>(d_pos, N, g, d_start, d_sorted, n, q0, nq, d_out);
+    ck(cudaGetLastError(), "query");
+    ck(cudaMemcpyAsync(neighbors_out + q0 * n, d_out, sizeof(long long) * nq * n, cudaMemcpyDeviceToHost, st),
+       "download");
+    ck(cudaStreamSynchronize(st), "knn");
+  }
+  cudaFreeAsync(d_pos, st);
+  cudaFreeAsync(d_cell, st);
+  cudaFreeAsync(d_sorted, st);
+  cudaFreeAsync(d_count, st);
+  cudaFreeAsync(d_start, st);
+  cudaFreeAsync(d_out, st);
+  if (d_tmp) cudaFreeAsync(d_tmp, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return rc;
 }
 
 int rbf_plan_weight_row_sum_max(rbf_plan* p, double* out) {

@@ -141,13 +141,22 @@ def laplacian_weights(nodes: NodeSet, stencils: StencilSet, degree: int,
     return ShapeStore(degree=degree, interior_nodes=interior, weights=weights, stencils=stencils)
 
 
-def synthetic_problem(target: int, n: int, degree: int, seed: int = 1, weights: str = "cpu"):
+def synthetic_problem(target: int, n: int, degree: int, seed: int = 1, weights: str = "cpu",
+                      knn: str | None = None):
     """(nodes, stencils, shapes) of a synthetic scattered-node disk.
 
     weights="cpu": numpy/LAPACK restatement above; "gpu": the device assembly
-    (paper_2107_03632_b200.weights, minutes -> seconds at 1e7 rows)."""
+    (paper_2107_03632_b200.weights, minutes -> seconds at 1e7 rows).
+    knn="cpu": scipy cKDTree; "gpu": the exact device kNN (default when the
+    weights are assembled on the GPU)."""
     nodes = disk_nodes(target, seed)
-    stencils = knn_stencils(nodes, n)
+    knn = knn or ("gpu" if weights == "gpu" else "cpu")
+    if knn == "gpu":
+        from .neighborhoods import build_stencils
+
+        stencils = build_stencils(nodes, n)
+    else:
+        stencils = knn_stencils(nodes, n)
     if weights == "gpu":
         from .weights import assemble_shapes
 
