@@ -3,7 +3,7 @@
 node-updates/s, and the fraction of the HBM roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c1|c3|c4|c2x10] [--native] [--ldg] [--quick]
+                    [--workload c2|c1|c3|c4|c5|c2x10] [--native] [--ldg] [--quick]
 
 One bench "step" is one pseudo-time iteration over every interior row (one
 pass of the hot path, solver.py:198-217); a node-update is one interior row in
@@ -44,6 +44,7 @@ WORKLOADS = {
     "c3": (10_000_000, 30, 4, "C3: m=4 n=30 N=1e7 synthetic scattered disk, fp64, 1xB200"),
     "c2x10": (10_000_000, 15, 2, "m=2 n=15 N=1e7 synthetic scattered disk, fp64, 1xB200 (north-star m=2 at N>=1e7)"),
     "c4": (25_000_000, 56, 6, "C4: m=6 n=56 N=2.5e7 synthetic scattered disk, fp64, 1xB200"),
+    "c5": (100_000_000, 56, 6, "C5: m=6 n=56 N=1e8 synthetic scattered disk, fp64, 1xB200 (single-GPU base of the 2/4/8-GPU config)"),
 }
 
 
@@ -51,15 +52,18 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def build_problem(workload: str, seed: int = 1):
+def build_problem(workload: str, seed: int = 1, gpu_setup: bool = True):
+    """The workload's (nodes, stencils, shapes).  gpu_setup: exact kNN and
+    weights on the GPU; False (the --impl reference arm) keeps the whole setup
+    on the CPU (cKDTree, numpy/LAPACK weights) so that arm runs no GPU code."""
     import paper_2107_03632_b200 as rb
     from paper_2107_03632_b200 import synth
 
     target, n, m, _ = WORKLOADS[workload]
     if workload == "c1":
         return rb.load_fixture(ROOT / "tests" / "golden" / "dome.npz")
-    # nodes + kNN on the CPU (scipy), weights assembled on the GPU
-    return synth.synthetic_problem(target, n, m, seed=seed, weights="gpu")
+    return synth.synthetic_problem(target, n, m, seed=seed, weights="gpu" if gpu_setup else "cpu",
+                                   knn="gpu" if gpu_setup else "cpu")
 
 
 def measured_peak():
@@ -171,11 +175,9 @@ def run_reference(args, workload):
     from oracle import oracle as orc
 
     t0 = time.perf_counter()
-    nodes, _, shapes = build_problem(workload)
+    nodes, _, shapes = build_problem(workload, gpu_setup=False)
     log(f"[ref] setup {time.perf_counter() - t0:.1f}s N={nodes.n_total} N_i={shapes.n_rows}")
-    import paper_2107_03632_b200 as rb
-
-    dt = 0.5 * rb.stability_bound(shapes)
+    dt = 0.5 * orc.stability_bound(shapes.weights)  # solver.py:188, :249-254
     interior = shapes.interior_nodes
     rows = np.ascontiguousarray(shapes.stencils.neighbors[interior])
     f_int = np.ascontiguousarray(orc.forcing(nodes.positions[interior]))
@@ -300,6 +302,8 @@ def main():
         f"{achieved_gbs:.0f} GB/s algorithmic ({achieved_gbs / peak:.3f} of {peak_src}); "
         f"residual {res.residual}")
 
+    plan_info = info
+    plan.close()  # the e2e leg builds its own plan (C5: ~70 GB of HBM each)
     # ---- end to end through the public API (host arrays in, host field out)
     cfg = rb.SolveConfig(degree=int(shapes.degree), support_size=n, nodes=int(nodes.n_total),
                          dt=dt, steps=args.steps)
@@ -380,7 +384,7 @@ def main():
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
-    plan.close()
+    del plan_info
     return 0
 
 
