@@ -34,7 +34,6 @@
 #include <limits>
 #include <memory>
 #include <mutex>
-#include <parallel/algorithm>
 #include <string>
 #include <vector>
 
@@ -166,18 +165,6 @@ cudaError_t set_max_smem(F fn) {
                               optin - static_cast<int>(fa.sharedSizeBytes));
 }
 
-uint64_t morton2(uint32_t x, uint32_t y) {
-  auto spread = [](uint64_t v) {
-    v &= 0x1fffffull;
-    v = (v | (v << 32)) & 0x1f00000000ffffull;
-    v = (v | (v << 16)) & 0x1f0000ff0000ffull;
-    v = (v | (v << 8)) & 0x100f00f00f00f00full;
-    v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
-    v = (v | (v << 2)) & 0x1249249249249249ull;
-    return v;
-  };
-  return spread(x) | (spread(y) << 1);
-}
 
 }  // namespace
 
@@ -899,55 +886,37 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   if (assemble) RBF_TRY(fill_monomials(degree, &wproto));
   if (assemble && n < wproto.M) return fail(RBF_ERR_PARAM, "support size below the monomial count");
 
-  // ---- host-side validation + renumbering ----------------------------------
+  // ---- validation (host, parallel: parameter errors before any CUDA call) ----
   PhaseTimer timer;
   const int64_t B = N - N_i;
   std::vector<uint8_t> seen(static_cast<size_t>(N), 0);
-  bool identity = !morton;
+  int bad_range = 0, bad_dup = 0, ident = morton ? 0 : 1;
+#pragma omp parallel for schedule(static) reduction(| : bad_range, bad_dup) reduction(& : ident)
   for (int64_t k = 0; k < N_i; ++k) {
     const int64_t v = interior[k];
-    if (v < 0 || v >= N) return fail(RBF_ERR_PARAM, "interior node id out of range");
-    if (seen[v]) return fail(RBF_ERR_PARAM, "interior node ids must be distinct");
-    seen[v] = 1;
-    if (v != B + k) identity = false;
-  }
-  std::vector<int64_t> row_of_k;  // k -> plan row (empty: identity)
-  std::vector<int32_t> new_id;    // original node -> plan node (empty: identity)
-  if (!identity) {
-    std::vector<int64_t> order(static_cast<size_t>(N_i));
-    for (int64_t k = 0; k < N_i; ++k) order[k] = k;
-    if (morton && N_i > 1) {
-      double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
-      for (int64_t i = 0; i < N; ++i) {
-        xmin = std::min(xmin, positions[2 * i]);
-        xmax = std::max(xmax, positions[2 * i]);
-        ymin = std::min(ymin, positions[2 * i + 1]);
-        ymax = std::max(ymax, positions[2 * i + 1]);
-      }
-      const double sx = (xmax > xmin) ? 2097151.0 / (xmax - xmin) : 0.0;
-      const double sy = (ymax > ymin) ? 2097151.0 / (ymax - ymin) : 0.0;
-      std::vector<uint64_t> code(static_cast<size_t>(N_i));
-#pragma omp parallel for schedule(static)
-      for (int64_t k = 0; k < N_i; ++k) {
-        const int64_t v = interior[k];
-        const uint32_t qx = static_cast<uint32_t>((positions[2 * v] - xmin) * sx);
-        const uint32_t qy = static_cast<uint32_t>((positions[2 * v + 1] - ymin) * sy);
-        code[k] = morton2(qx, qy);
-      }
-      __gnu_parallel::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-        return code[a] < code[b] || (code[a] == code[b] && a < b);
-      });
+    if (v < 0 || v >= N) {
+      bad_range = 1;
+    } else if (__atomic_fetch_or(&seen[v], static_cast<uint8_t>(1), __ATOMIC_RELAXED)) {
+      bad_dup = 1;
     }
-    row_of_k.resize(static_cast<size_t>(N_i));
-    for (int64_t r = 0; r < N_i; ++r) row_of_k[order[r]] = r;
-    new_id.assign(static_cast<size_t>(N), -1);
-    int32_t next = 0;
-    for (int64_t i = 0; i < N; ++i)
-      if (!seen[i]) new_id[i] = next++;
-    for (int64_t k = 0; k < N_i; ++k) new_id[interior[k]] = static_cast<int32_t>(B + row_of_k[k]);
+    if (v != B + k) ident = 0;
   }
-  seen.clear();
-  seen.shrink_to_fit();
+  if (bad_range) return fail(RBF_ERR_PARAM, "interior node id out of range");
+  if (bad_dup) return fail(RBF_ERR_PARAM, "interior node ids must be distinct");
+  const bool identity = ident != 0;
+  double xmin = 0, xmax = 0, ymin = 0, ymax = 0;
+  if (morton && N_i > 1) {
+    double a0 = 1e300, a1 = -1e300, b0 = 1e300, b1 = -1e300;
+#pragma omp parallel for schedule(static) reduction(min : a0, b0) reduction(max : a1, b1)
+    for (int64_t i = 0; i < N; ++i) {
+      a0 = std::min(a0, positions[2 * i]);
+      a1 = std::max(a1, positions[2 * i]);
+      b0 = std::min(b0, positions[2 * i + 1]);
+      b1 = std::max(b1, positions[2 * i + 1]);
+    }
+    xmin = a0, xmax = a1, ymin = b0, ymax = b1;
+  }
+  timer.mark("validate (host)");
   timer.mark("validate + renumber (host)");
 
   std::unique_ptr<rbf_plan> p(new rbf_plan());
@@ -981,16 +950,69 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   // ---- device-side SELL-32 packing, in row chunks through pinned staging ----
   long long* d_row_of_k = nullptr;
   if (!identity) {
+    // ---- renumbering on the device: Morton keys, stable radix sort, maps ----
     RBF_TRY(dev_alloc(p.get(), &p->new_id, static_cast<size_t>(N)));
     RBF_TRY(dev_alloc(p.get(), &p->tmp, static_cast<size_t>(N)));
-    RBF_CK(cudaMemcpyAsync(p->new_id, new_id.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, p->stream));
-    if (N_i > 0) {
-      RBF_TRY(dev_alloc(p.get(), &p->row_of_k, static_cast<size_t>(N_i)));
-      d_row_of_k = p->row_of_k;
-      RBF_CK(cudaMemcpyAsync(d_row_of_k, row_of_k.data(), sizeof(long long) * N_i, cudaMemcpyHostToDevice,
-                             p->stream));
+    RBF_TRY(dev_alloc(p.get(), &p->row_of_k, static_cast<size_t>(std::max<int64_t>(1, N_i))));
+    d_row_of_k = p->row_of_k;
+    long long* d_int = nullptr;
+    unsigned char* d_seen = nullptr;
+    int* d_flag = nullptr;
+    RBF_TRY(pool_alloc(&d_int, static_cast<size_t>(std::max<int64_t>(1, N_i)), p->stream));
+    RBF_TRY(pool_alloc(&d_seen, static_cast<size_t>(N), p->stream));
+    RBF_TRY(pool_alloc(&d_flag, static_cast<size_t>(N), p->stream));
+    RBF_CK(cudaMemcpyAsync(d_int, interior, sizeof(long long) * N_i, cudaMemcpyHostToDevice, p->stream));
+    RBF_CK(cudaMemcpyAsync(d_seen, seen.data(), N, cudaMemcpyHostToDevice, p->stream));
+    const int blocks = static_cast<int>(std::min<int64_t>((std::max(N, N_i) + 255) / 256, 148 * 16));
+    long long* d_order = nullptr;
+    RBF_TRY(pool_alloc(&d_order, static_cast<size_t>(std::max<int64_t>(1, N_i)), p->stream));
+    if (morton && N_i > 1) {
+      double* d_pos = nullptr;
+      unsigned long long *d_key = nullptr, *d_key2 = nullptr;
+      long long* d_val = nullptr;
+      RBF_TRY(pool_alloc(&d_pos, static_cast<size_t>(2 * N), p->stream));
+      RBF_TRY(pool_alloc(&d_key, static_cast<size_t>(N_i), p->stream));
+      RBF_TRY(pool_alloc(&d_key2, static_cast<size_t>(N_i), p->stream));
+      RBF_TRY(pool_alloc(&d_val, static_cast<size_t>(N_i), p->stream));
+      RBF_CK(cudaMemcpyAsync(d_pos, positions, sizeof(double) * 2 * N, cudaMemcpyHostToDevice, p->stream));
+      const double sx = (xmax > xmin) ? 2097151.0 / (xmax - xmin) : 0.0;
+      const double sy = (ymax > ymin) ? 2097151.0 / (ymax - ymin) : 0.0;
+      rbf::morton_keys_kernel<<<blocks, 256, 0, p->stream>>>(d_pos, d_int, N_i, xmin, ymin, sx, sy, d_key, d_val);
+      RBF_CK(cudaGetLastError());
+      size_t tb = 0;
+      RBF_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, d_key, d_key2, d_val, d_order, N_i, 0, 42, p->stream));
+      void* d_tb = nullptr;
+      RBF_TRY(pool_alloc(reinterpret_cast<unsigned char**>(&d_tb), std::max<size_t>(tb, 16), p->stream));
+      RBF_CK(cub::DeviceRadixSort::SortPairs(d_tb, tb, d_key, d_key2, d_val, d_order, N_i, 0, 42, p->stream));
+      pool_free(d_tb, p->stream);
+      pool_free(d_pos, p->stream);
+      pool_free(d_key, p->stream);
+      pool_free(d_key2, p->stream);
+      pool_free(d_val, p->stream);
+    } else {
+      rbf::iota_kernel<<<blocks, 256, 0, p->stream>>>(d_order, N_i);
+      RBF_CK(cudaGetLastError());
     }
+    // row_of_k[order[r]] = r;  new_id: non-interior nodes keep their relative
+    // order at 0..B-1 (exclusive scan of !seen), interior node k -> B + row_of_k[k]
+    rbf::invert_order_kernel<<<blocks, 256, 0, p->stream>>>(d_order, N_i, d_row_of_k);
+    rbf::not_seen_kernel<<<blocks, 256, 0, p->stream>>>(d_seen, N, d_flag);
+    RBF_CK(cudaGetLastError());
+    size_t tb = 0;
+    RBF_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, d_flag, p->new_id, static_cast<int>(N), p->stream));
+    void* d_tb = nullptr;
+    RBF_TRY(pool_alloc(reinterpret_cast<unsigned char**>(&d_tb), std::max<size_t>(tb, 16), p->stream));
+    RBF_CK(cub::DeviceScan::ExclusiveSum(d_tb, tb, d_flag, p->new_id, static_cast<int>(N), p->stream));
+    rbf::interior_ids_kernel<<<blocks, 256, 0, p->stream>>>(d_int, d_row_of_k, N_i, B, p->new_id);
+    RBF_CK(cudaGetLastError());
+    pool_free(d_tb, p->stream);
+    pool_free(d_order, p->stream);
+    pool_free(d_int, p->stream);
+    pool_free(d_seen, p->stream);
+    pool_free(d_flag, p->stream);
   }
+  seen.clear();
+  seen.shrink_to_fit();
   int* d_err = nullptr;
   RBF_TRY(pool_alloc(&d_err, 1, p->stream));
   RBF_CK(cudaMemsetAsync(d_err, 0, sizeof(int), p->stream));

@@ -1043,6 +1043,53 @@ __global__ void row_abs_sum_max_kernel(const double* __restrict__ W, long long n
   if ((threadIdx.x & 31) == 0 && m) atomicMax(reinterpret_cast<unsigned long long*>(out), m);
 }
 
+// ---- renumbering (plan build) -----------------------------------------------
+__device__ __forceinline__ unsigned long long spread_bits21(unsigned long long v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x1f00000000ffffull;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+// key[k] = Morton code of interior node k's position (21 bits per axis over
+// the bounding box), val[k] = k; a stable radix sort of (key, val) orders the
+// rows by (code, k)
+__global__ void morton_keys_kernel(const double* __restrict__ pos, const long long* __restrict__ interior,
+                                   long long n_rows, double xmin, double ymin, double sx, double sy,
+                                   unsigned long long* __restrict__ key, long long* __restrict__ val) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n_rows;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long v = interior[k];
+    const unsigned long long qx = static_cast<unsigned int>((pos[2 * v] - xmin) * sx);
+    const unsigned long long qy = static_cast<unsigned int>((pos[2 * v + 1] - ymin) * sy);
+    key[k] = spread_bits21(qx) | (spread_bits21(qy) << 1);
+    val[k] = k;
+  }
+}
+__global__ void iota_kernel(long long* __restrict__ out, long long n) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[k] = k;
+}
+__global__ void invert_order_kernel(const long long* __restrict__ order, long long n, long long* __restrict__ row_of_k) {
+  for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < n;
+       r += static_cast<long long>(gridDim.x) * blockDim.x)
+    row_of_k[order[r]] = r;
+}
+__global__ void not_seen_kernel(const unsigned char* __restrict__ seen, long long n, int* __restrict__ flag) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    flag[i] = seen[i] ? 0 : 1;
+}
+__global__ void interior_ids_kernel(const long long* __restrict__ interior, const long long* __restrict__ row_of_k,
+                                    long long n_rows, long long B, int* __restrict__ new_id) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n_rows;
+       k += static_cast<long long>(gridDim.x) * blockDim.x)
+    new_id[interior[k]] = static_cast<int>(B + row_of_k[k]);
+}
+
 // F[row_of_k[k]] = f[k]
 __global__ void scatter_rows_kernel(const double* __restrict__ f, const long long* __restrict__ row_of_k,
                                     long long n_rows, double* __restrict__ F) {
