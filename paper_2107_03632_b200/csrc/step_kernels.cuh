@@ -1044,13 +1044,14 @@ __global__ void row_abs_sum_max_kernel(const double* __restrict__ W, long long n
 }
 
 // ---- renumbering (plan build) -----------------------------------------------
+// 2-D bit interleave of a 21-bit coordinate: bit i -> bit 2i
 __device__ __forceinline__ unsigned long long spread_bits21(unsigned long long v) {
   v &= 0x1fffffull;
-  v = (v | (v << 32)) & 0x1f00000000ffffull;
-  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
-  v = (v | (v << 8)) & 0x100f00f00f00f00full;
-  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
-  v = (v | (v << 2)) & 0x1249249249249249ull;
+  v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+  v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
   return v;
 }
 // key[k] = Morton code of interior node k's position (21 bits per axis over

@@ -47,13 +47,13 @@ def morton_codes(xy: np.ndarray) -> np.ndarray:
     span[span == 0] = 1.0
     q = ((xy - lo) * (2097151.0 / span)).astype(np.uint64)
 
-    def spread(v):
+    def spread(v):  # 2-D bit interleave: bit i -> bit 2i
         v = v & np.uint64(0x1FFFFF)
-        v = (v | (v << np.uint64(32))) & np.uint64(0x1F00000000FFFF)
-        v = (v | (v << np.uint64(16))) & np.uint64(0x1F0000FF0000FF)
-        v = (v | (v << np.uint64(8))) & np.uint64(0x100F00F00F00F00F)
-        v = (v | (v << np.uint64(4))) & np.uint64(0x10C30C30C30C30C3)
-        v = (v | (v << np.uint64(2))) & np.uint64(0x1249249249249249)
+        v = (v | (v << np.uint64(16))) & np.uint64(0x0000FFFF0000FFFF)
+        v = (v | (v << np.uint64(8))) & np.uint64(0x00FF00FF00FF00FF)
+        v = (v | (v << np.uint64(4))) & np.uint64(0x0F0F0F0F0F0F0F0F)
+        v = (v | (v << np.uint64(2))) & np.uint64(0x3333333333333333)
+        v = (v | (v << np.uint64(1))) & np.uint64(0x5555555555555555)
         return v
 
     return spread(q[:, 0]) | (spread(q[:, 1]) << np.uint64(1))

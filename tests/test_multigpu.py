@@ -58,6 +58,9 @@ def test_morton_codes_order_locality():
     xy = np.array([[0.0, 0.0], [1.0, 1.0], [0.0, 1.0], [1.0, 0.0]])
     c = morton_codes(xy)
     assert c[0] < c[3] < c[2] < c[1]  # z-order: (0,0) (1,0) (0,1) (1,1)
+    rng = np.random.default_rng(3)
+    c = morton_codes(rng.uniform(size=(1000, 2)))
+    assert int(c.max()) < 2**42  # 21 bits per axis, interleaved
 
 
 def _emulate(parts, u0, dt, steps):

@@ -592,3 +592,34 @@ def test_plan_file_round_trip_is_bitwise(golden, synth_cache, tmp_path, which):
     trunc.write_bytes(path.read_bytes()[:200])
     with pytest.raises(rb.ParameterError):
         Plan.load(trunc)
+
+
+def test_device_morton_renumbering_is_the_z_order(synth_cache, tmp_path):
+    """The plan's row order must be the (Morton code, k) order over the
+    bounding box of all nodes (a wrong order keeps bitwise parity but loses
+    the locality the 16-bit ids and the gathers rely on)."""
+    import struct
+
+    from paper_2107_03632_b200.multigpu import morton_codes
+
+    nodes, _, shapes = _synth(synth_cache, 30_000, 15, 2)
+    interior = shapes.interior_nodes
+    plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                rb.forcing(nodes.positions[interior]), nodes.positions, renumber=True)
+    path = tmp_path / "p.rbf"
+    plan.save(path)
+    raw = path.read_bytes()
+    fmt = "<8sii4qii5q"
+    _, _, n, N, N_i, B, S, ib, ren, _ = struct.unpack(fmt, raw[:struct.calcsize(fmt)])[:10]
+    off = struct.calcsize(fmt) + S * 32 * n * 12 + S * 32 * 8 + (S * 32 * n * 2 + S * 16 if ib == 16 else 0)
+    new_id = np.frombuffer(raw, dtype=np.int32, count=N, offset=off)
+    row_of_k = np.frombuffer(raw, dtype=np.int64, count=N_i, offset=off + 4 * N)
+    xy = nodes.positions
+    lo, span = xy.min(0), xy.max(0) - xy.min(0)
+    codes = morton_codes(np.vstack([xy[interior], lo, lo + span]))[:-2]  # same box as the library
+    order = np.lexsort((np.arange(N_i), codes))
+    want = np.empty(N_i, np.int64)
+    want[order] = np.arange(N_i)
+    assert ren == 1 and np.array_equal(row_of_k, want)
+    assert np.array_equal(new_id[interior], B + want)
+    assert np.array_equal(np.sort(new_id[~np.isin(np.arange(N), interior)]), np.arange(B))
