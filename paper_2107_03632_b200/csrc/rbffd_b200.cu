@@ -275,6 +275,43 @@ int dev_alloc(rbf_plan* p, T** ptr, size_t count) {
   return RBF_OK;
 }
 
+// Pinned host status slots for all plans of the process: one pinned slab,
+// handed out from a free list (cudaMallocHost / cudaFreeHost per plan cost up
+// to ~40 ms at plan teardown, profiles/README.md).
+struct StatusSlab {
+  std::mutex mu;
+  std::vector<rbf::DevStatus*> free_list;
+  std::vector<void*> slabs;
+};
+
+StatusSlab& status_slab() {
+  static StatusSlab s;
+  return s;
+}
+
+cudaError_t status_alloc(rbf::DevStatus** out) {
+  StatusSlab& sl = status_slab();
+  std::lock_guard<std::mutex> lock(sl.mu);
+  if (sl.free_list.empty()) {
+    constexpr int kSlots = 256;
+    void* mem = nullptr;
+    cudaError_t e = cudaMallocHost(&mem, sizeof(rbf::DevStatus) * kSlots);
+    if (e != cudaSuccess) return e;
+    sl.slabs.push_back(mem);
+    for (int i = kSlots - 1; i >= 0; --i) sl.free_list.push_back(static_cast<rbf::DevStatus*>(mem) + i);
+  }
+  *out = sl.free_list.back();
+  sl.free_list.pop_back();
+  return cudaSuccess;
+}
+
+void status_free(rbf::DevStatus* p) {
+  if (!p) return;
+  StatusSlab& sl = status_slab();
+  std::lock_guard<std::mutex> lock(sl.mu);
+  sl.free_list.push_back(p);
+}
+
 // Pinned, double-buffered staging for plan uploads: the host copies (and
 // int64 -> int32 id conversion) of chunk c+1 run while chunk c is on the bus.
 struct Staging {
@@ -933,7 +970,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   RBF_CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   RBF_CK(cudaEventCreate(&p->ev0));
   RBF_CK(cudaEventCreate(&p->ev1));
-  RBF_CK(cudaMallocHost(reinterpret_cast<void**>(&p->h_st), sizeof(rbf::DevStatus)));
+  RBF_CK(status_alloc(&p->h_st));
   RBF_TRY(dev_alloc(p.get(), &p->st, 1));
   const size_t sell = static_cast<size_t>(p->S) * 32 * n;
   RBF_TRY(dev_alloc(p.get(), &p->W, sell));
@@ -1419,7 +1456,7 @@ int rbf_plan_load(rbf_plan** out, const char* path, int32_t device, uint32_t fla
     step(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) == cudaSuccess ? RBF_OK : fail(RBF_ERR_CUDA, "stream"));
     step(cudaEventCreate(&p->ev0) == cudaSuccess ? RBF_OK : fail(RBF_ERR_CUDA, "event"));
     step(cudaEventCreate(&p->ev1) == cudaSuccess ? RBF_OK : fail(RBF_ERR_CUDA, "event"));
-    step(cudaMallocHost(reinterpret_cast<void**>(&p->h_st), sizeof(rbf::DevStatus)) == cudaSuccess
+    step(status_alloc(&p->h_st) == cudaSuccess
              ? RBF_OK : fail(RBF_ERR_CUDA, "host status"));
   }
   const size_t sell = static_cast<size_t>(p->S) * 32 * p->n;
@@ -1688,7 +1725,7 @@ void rbf_plan_destroy(rbf_plan* p) {
   pool_free(p->halo_sendbuf, s);
   pool_free(p->st, s);
   if (s) cudaStreamSynchronize(s);
-  if (p->h_st) cudaFreeHost(p->h_st);
+  status_free(p->h_st);
   if (p->ev0) cudaEventDestroy(p->ev0);
   if (p->ev1) cudaEventDestroy(p->ev1);
   if (p->stream) cudaStreamDestroy(p->stream);

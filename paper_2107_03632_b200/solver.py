@@ -434,6 +434,7 @@ def run_time_loop(config: SolveConfig, nodes, shapes, copy_back: bool = False, *
     """
     if renumber is None:
         renumber = shapes.n_rows >= RENUMBER_MIN_ROWS
+    tick = _Ticker()
     interior = shapes.interior_nodes
     # sin(pi x) sin(pi y) is evaluated once for the forcing (geometry.py:84-86),
     # the Dirichlet values (solver.py:130-138) and the error norms
@@ -443,12 +444,15 @@ def run_time_loop(config: SolveConfig, nodes, shapes, copy_back: bool = False, *
     u1 = np.zeros(nodes.n_total)  # solver.py:186
     bidx = nodes.boundary_indices
     u1[bidx] = exact[bidx]
+    tick("host prep (closed form, forcing, Dirichlet)")
     dt = config.dt if config.dt is not None else _AUTO_DT_SAFETY * stability_bound(shapes)
     plan = _plan_for(shapes, nodes.n_total, f_int, nodes.positions if renumber else None,
                      cache=cache, renumber=renumber)
+    tick("plan")
     plan.set_field(u1)
     res = plan.run(dt, steps=config.steps, mode=config.mode, tol=config.tol,
                    max_steps=config.max_steps, copy_back=copy_back)
+    tick("set_field + run")
     if res.status == _lib.RBF_ERR_INSTABILITY:
         u2 = plan.get_field()
         max_abs = float(np.max(np.abs(u2)))
@@ -464,9 +468,12 @@ def run_time_loop(config: SolveConfig, nodes, shapes, copy_back: bool = False, *
             residual=res.residual,
         )
     field_ = plan.get_field()
+    tick("get_field")
     if not cache:
         plan.close()
+    tick("plan close")
     linf, l2 = _norms(field_, exact)
+    tick("norms")
     return SolveReport(
         field=field_,
         steps=res.steps_done,
@@ -477,6 +484,24 @@ def run_time_loop(config: SolveConfig, nodes, shapes, copy_back: bool = False, *
         config=config.as_dict(dt_effective=dt),
         device_seconds=res.device_seconds,
     )
+
+
+class _Ticker:
+    """RBFFD_VERBOSE=1: phase times of run_time_loop on stderr."""
+
+    def __init__(self):
+        import os
+
+        self.on = bool(os.environ.get("RBFFD_VERBOSE"))
+        self.t = time.perf_counter()
+
+    def __call__(self, what: str) -> None:
+        if self.on:
+            import sys
+
+            t = time.perf_counter()
+            print(f"[rbffd.py] {what:<44s} {1e3 * (t - self.t):8.2f} ms", file=sys.stderr, flush=True)
+            self.t = t
 
 
 def _norms(values: np.ndarray, exact: np.ndarray):
