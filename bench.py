@@ -8,8 +8,11 @@ node-updates/s, and the fraction of the HBM roofline).
 One bench "step" is one pseudo-time iteration over every interior row (one
 pass of the hot path, solver.py:198-217); a node-update is one interior row in
 one step (perf.py:74).  Default workload: BASELINE config 2 -- m=2, n=15,
-N=1e6 scattered nodes, fp64, one B200 -- on a synthetic scattered-node disk
-(paper_2107_03632_b200/synth.py; the GPU box has no reference package).
+N=1e6 scattered nodes, fp64, one B200 -- on the reference's own
+advancing-front node set for target 1e6, seed 1 (N=1,046,538, N_i=1,042,999,
+SURVEY.md 8d), regenerated bit-identically by the native generator
+(paper_2107_03632_b200/geometry.py; the GPU box has no reference package),
+with exact GPU kNN supports and GPU-assembled PHS+poly weights.
 
 `value` is device throughput with all inputs resident in HBM (CUDA events on
 the plan's stream around exactly K steps, max over ranks); `e2e` is the same
@@ -40,11 +43,11 @@ METRIC = "node-updates/s of RBF-FD Poisson explicit loop at m=2/4/6; % HBM roofl
 WORKLOADS = {
     # name: (target N, n, m, description)
     "c1": (1027, 15, 2, "C1: paper Fig. 1 case, m=2 n=15 N=1027 (golden fixture, reference nodes)"),
-    "c2": (1_000_000, 15, 2, "C2: m=2 n=15 N=1e6 synthetic scattered disk, fp64, 1xB200"),
-    "c3": (10_000_000, 30, 4, "C3: m=4 n=30 N=1e7 synthetic scattered disk, fp64, 1xB200"),
-    "c2x10": (10_000_000, 15, 2, "m=2 n=15 N=1e7 synthetic scattered disk, fp64, 1xB200 (north-star m=2 at N>=1e7)"),
-    "c4": (25_000_000, 56, 6, "C4: m=6 n=56 N=2.5e7 synthetic scattered disk, fp64, 1xB200"),
-    "c5": (100_000_000, 56, 6, "C5: m=6 n=56 N=1e8 synthetic scattered disk, fp64, 1xB200 (single-GPU base of the 2/4/8-GPU config)"),
+    "c2": (1_000_000, 15, 2, "C2: m=2 n=15 N=1e6 reference advancing-front disk (seed 1), fp64, 1xB200"),
+    "c3": (10_000_000, 30, 4, "C3: m=4 n=30 N=1e7 reference advancing-front disk (seed 1), fp64, 1xB200"),
+    "c2x10": (10_000_000, 15, 2, "m=2 n=15 N=1e7 reference advancing-front disk (seed 1), fp64, 1xB200 (north-star m=2 at N>=1e7)"),
+    "c4": (25_000_000, 56, 6, "C4: m=6 n=56 N=2.5e7 reference advancing-front disk (seed 1), fp64, 1xB200"),
+    "c5": (100_000_000, 56, 6, "C5: m=6 n=56 N=1e8 reference advancing-front disk (seed 1), fp64, 1xB200 (single-GPU base of the 2/4/8-GPU config)"),
 }
 
 
@@ -206,7 +209,8 @@ def run_reference(args, workload):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic" if workload != "c1" else "reference fixture (tests/golden/dome.npz)",
+        "data": ("synthetic (reference advancing-front nodes via the native generator, GPU kNN + weights)"
+                 if workload != "c1" else "reference fixture (tests/golden/dome.npz)"),
         "config": {"workload": WORKLOADS[workload][3], "N": int(nodes.n_total),
                    "N_i": int(interior.size), "n": int(shapes.weights.shape[1]),
                    "m": int(shapes.degree), "dt": dt},
@@ -340,7 +344,8 @@ def main():
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic" if args.workload != "c1" else "reference fixture",
+        "data": ("synthetic (reference advancing-front nodes via the native generator)"
+                 if args.workload != "c1" else "reference fixture"),
         "config": {
             "workload": WORKLOADS[args.workload][3],
             "N": int(nodes.n_total), "N_i": N_i, "n": n, "m": int(shapes.degree), "dt": dt,

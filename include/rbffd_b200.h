@@ -108,6 +108,21 @@ int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows
  */
 int rbf_knn(const double* positions, int64_t N, int32_t n, int64_t* neighbors_out, int32_t device);
 
+/*
+ * The reference's advancing-front node set on the unit disk (SURVEY.md §8f
+ * row 4; rbffd.geometry.generate_unit_disk_nodes, geometry.py:105-198),
+ * bit-identical: same MT19937 candidate-angle stream, same acceptance order,
+ * same IEEE operations.  Host code (the algorithm is sequential by
+ * construction; a parallel acceptance rule would change the node set).
+ * seed_key[key_len] are the 32-bit little-endian words of |seed| as CPython's
+ * random.seed(int) uses them (one zero word for seed 0).  On success
+ * *positions_out is a malloc'd [N*2] array (boundary ring first, then the
+ * interior in acceptance order) to be released with rbf_free_host.
+ */
+int rbf_generate_unit_disk_nodes(double h, const uint32_t* seed_key, int32_t key_len,
+                                 double** positions_out, int64_t* n_total, int64_t* n_boundary);
+void rbf_free_host(void* p);
+
 /* rbf_plan_create with the weights assembled on the device straight into the
  * SELL layout (the host never holds them; positions are required). */
 int rbf_plan_create_assembled(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, int32_t degree,

@@ -2,7 +2,7 @@
 loop with NCCL halo exchange (multigpu.NcclGroup).
 
 Weak scaling: each GPU holds one BASELINE-config-2-sized share (N = 1e6 per
-GPU, m=2, n=15) of one synthetic disk of N x world nodes; value = all ranks'
+GPU, m=2, n=15) of the reference's advancing-front disk of N x world nodes; value = all ranks'
 node-updates / max-over-ranks device time.  Each rank assembles only the
 weights of its own rows.  torch.distributed (gloo) is the control plane
 (NCCL id broadcast, barriers, max over ranks); the halos and the per-step
@@ -36,7 +36,11 @@ def main(args, metric, workloads):  # pragma: no cover - needs >1 GPU
     target_per_gpu, n, m, desc = workloads[args.workload]
     target = target_per_gpu * world
     t0 = time.perf_counter()
-    nodes = synth.disk_nodes(target, seed=1)
+    from .geometry import generate_unit_disk_nodes
+    from .problem import spacing_for_node_count
+
+    # the reference's advancing-front set, identical on every rank
+    nodes = generate_unit_disk_nodes(spacing_for_node_count(target), 1)
     st = synth.knn_stencils(nodes, n, workers=max(1, (os.cpu_count() or 1) // world))
     interior = nodes.interior_indices.astype(np.int64)
     rows = np.ascontiguousarray(st.neighbors[interior])

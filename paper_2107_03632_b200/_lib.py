@@ -56,6 +56,8 @@ EXPORTED = (
     "rbf_plan_save",
     "rbf_plan_load",
     "rbf_knn",
+    "rbf_generate_unit_disk_nodes",
+    "rbf_free_host",
 )
 
 
@@ -144,6 +146,8 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "rbf_plan_save": ([vp, ctypes.c_char_p], i32),
         "rbf_plan_load": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, u32], i32),
         "rbf_knn": ([vp, i64, i32, vp, i32], i32),
+        "rbf_generate_unit_disk_nodes": ([ctypes.c_double, vp, i32, vp, vp, vp], i32),
+        "rbf_free_host": ([vp], None),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

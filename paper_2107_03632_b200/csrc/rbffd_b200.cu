@@ -46,6 +46,15 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+}  // namespace
+
+namespace rbf_detail {
+// error entry for the host-only translation units (nodes.cpp)
+int fail_c(int code, const char* msg) { return fail(code, msg ? msg : ""); }
+}  // namespace rbf_detail
+
+namespace {
+
 #define RBF_CK(call)                                                                         \
   do {                                                                                       \
     cudaError_t e_ = (call);                                                                 \

@@ -115,13 +115,26 @@ def monomial_count(degree: int) -> int:
     return (degree + 1) * (degree + 2) // 2
 
 
+def _check_spacing(h: float) -> None:
+    """geometry.py:222-224."""
+    from .errors import ParameterError
+
+    if not (0.0 < h < 0.5):
+        raise ParameterError(f"spacing h={h} outside the valid range (0, 0.5)")
+
+
 def node_count_for_spacing(h: float) -> int:
     """geometry.py:89-95."""
+    _check_spacing(h)
     return int(math.floor(math.pi / h**2 + 2.0 * math.pi / h + 0.5))
 
 
 def spacing_for_node_count(n: int) -> float:
     """geometry.py:98-102 (inverse of node_count_for_spacing)."""
+    if n < 30:
+        from .errors import ParameterError
+
+        raise ParameterError(f"target node count {n} is too small (need >= 30)")
     return 1.0 / (math.sqrt(1.0 + n / math.pi) - 1.0)
 
 

@@ -1,10 +1,14 @@
-"""Synthetic scattered-node unit-disk domains for the benchmark configs.
+"""Scattered-node unit-disk domains for the benchmark configs.
 
-The reference's own setup (advancing-front nodes, geometry.py:105-198) takes
-~1 min per 1e6 nodes and hours at 1e7-1e8, and the GPU box has
-no reference package.  BASELINE.json therefore asks for throughput on
-"synthetic scattered-node domains"; SURVEY.md 8(d) names the accepted
-construction, implemented here:
+Nodes (``nodes=``):
+
+* ``"reference"`` (default): the reference's own advancing-front node set
+  (geometry.py:105-198) for (spacing_for_node_count(target), seed), produced
+  bit-identically by the native generator (geometry.generate_unit_disk_nodes,
+  csrc/nodes.cpp) -- ~1 s per 1e6 nodes instead of the Python original's
+  ~1 min, so C2..C5 run on the exact node sets SURVEY.md 8(d) prefers;
+* ``"hex"``: the faster fallback SURVEY.md 8(d) also accepts, a seeded jittered
+  hexagonal fill (disk_nodes below):
 
 * boundary: the reference's equidistant ring, same formula
   (n_b = floor(2 pi / h + 0.5), theta_k = 2 pi k / n_b; geometry.py:135-141);
@@ -142,14 +146,22 @@ def laplacian_weights(nodes: NodeSet, stencils: StencilSet, degree: int,
 
 
 def synthetic_problem(target: int, n: int, degree: int, seed: int = 1, weights: str = "cpu",
-                      knn: str | None = None):
+                      knn: str | None = None, nodes: str = "reference"):
     """(nodes, stencils, shapes) of a synthetic scattered-node disk.
 
     weights="cpu": numpy/LAPACK restatement above; "gpu": the device assembly
     (paper_2107_03632_b200.weights, minutes -> seconds at 1e7 rows).
     knn="cpu": scipy cKDTree; "gpu": the exact device kNN (default when the
-    weights are assembled on the GPU)."""
-    nodes = disk_nodes(target, seed)
+    weights are assembled on the GPU).  nodes="reference": the reference's
+    advancing-front set (native, bit-identical); "hex": jittered hex fill."""
+    if nodes == "reference":
+        from .geometry import generate_unit_disk_nodes
+
+        nodes = generate_unit_disk_nodes(spacing_for_node_count(target), seed)
+    elif nodes == "hex":
+        nodes = disk_nodes(target, seed)
+    else:
+        raise ValueError(f"nodes must be 'reference' or 'hex', got {nodes!r}")
     knn = knn or ("gpu" if weights == "gpu" else "cpu")
     if knn == "gpu":
         from .neighborhoods import build_stencils
