@@ -829,7 +829,9 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
     const size_t smem_t = 2 * 16 * sizeof(uint64_t) + static_cast<size_t>(stages) * stage;
     if (smem_t <= kResidentSmemMax && set_max_smem(tma_fn) == cudaSuccess) {
       p->tma_fn = tma_fn;
-      p->tma_geom = rbf::TmaGeom{sps, stages, std::getenv("RBFFD_TMA_CONTIG") ? 1 : 0};
+      p->tma_geom = rbf::TmaGeom{sps, stages, std::getenv("RBFFD_TMA_CONTIG") ? 1 : 0, 0};
+      p->tma_geom.res = (3 * stages) / 2;  // ring-fill chunks stay L2-resident (TmaGeom::res; sweep in profiles/README.md)
+      if (const char* e = std::getenv("RBFFD_L2_RES_CHUNKS")) p->tma_geom.res = std::atoll(e);
       p->tma_smem = smem_t;
       p->tma_block = 32 * (cw + 1);
       const int64_t chunks = (p->S + sps - 1) / sps;
