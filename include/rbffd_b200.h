@@ -55,6 +55,9 @@ extern "C" {
 #define RBF_NO_IDX16 0x20u        /* keep int32 node ids in the streamed step (no 16-bit windows) */
 #define RBF_FLOW 0x40u            /* opt-in: fixed-step runs in the persistent dataflow loop (measured
                                      slower than the graph path on B200, profiles/README.md) */
+#define RBF_NO_PAIR 0x80u         /* fixed-step runs one step per launch (no two-step tile kernel) */
+#define RBF_PAIR 0x100u           /* two-step tile kernel for fixed-step runs at any size (default:
+                                     only up to N_i*n = 1e6, where it is measured faster) */
 
 /* run modes (SolveConfig.mode, solver.py:53) */
 #define RBF_MODE_FIXED 0
@@ -208,6 +211,10 @@ typedef struct rbf_plan_info {
   int64_t bytes_per_step;  /* algorithmic HBM bytes per step: N_i*(12n+24) */
   int64_t launches;        /* kernel launches issued by this plan so far */
   int64_t stream_bytes_per_step; /* bytes the step actually streams (<= bytes_per_step with 16-bit ids) */
+  int32_t pair;            /* 1: fixed-step runs advance two steps per launch (tile-local
+                              temporal blocking, bitwise identical) */
+  int32_t pair_tiles;      /* its row tiles */
+  int64_t pair_halo_rows;  /* halo entries over all tiles (rows recomputed per launch) */
 } rbf_plan_info;
 
 int rbf_plan_get_info(const rbf_plan* plan, rbf_plan_info* info);

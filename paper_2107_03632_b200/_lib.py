@@ -27,6 +27,8 @@ RBF_STREAM_LDG = 0x8
 RBF_NO_CLUSTER = 0x10
 RBF_NO_IDX16 = 0x20
 RBF_FLOW = 0x40
+RBF_NO_PAIR = 0x80
+RBF_PAIR = 0x100
 
 RBF_MODE_FIXED = 0
 RBF_MODE_STEADY = 1
@@ -80,6 +82,9 @@ class PlanInfo(ctypes.Structure):
         ("bytes_per_step", ctypes.c_int64),
         ("launches", ctypes.c_int64),
         ("stream_bytes_per_step", ctypes.c_int64),
+        ("pair", ctypes.c_int32),
+        ("pair_tiles", ctypes.c_int32),
+        ("pair_halo_rows", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

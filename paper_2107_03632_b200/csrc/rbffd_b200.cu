@@ -16,6 +16,7 @@
 //    step (last-CTA ticket), so the host only polls a 64-byte status per chunk.
 #include "../../include/rbffd_b200.h"
 #include "step_kernels.cuh"
+#include "pair.h"
 #include "weights_kernels.cuh"
 #include "flow_kernels.cuh"
 #include "knn_kernels.cuh"
@@ -71,6 +72,7 @@ namespace {
 constexpr int kGraphSteps = 64;  // steps per captured graph (even: keeps buffer parity)
 constexpr int kStreamBlock = 256;
 constexpr size_t kResidentSmemMax = 227 * 1024;
+constexpr int64_t kPairAutoEntries = 1000000;  // N_i*n up to which fixed-step runs use the pair kernel
 
 using StreamFn = void (*)(rbf::StepArgs, const double*, double*, int);
 using TmaFn = void (*)(rbf::StepArgs, const double*, double*, int, rbf::TmaGeom);
@@ -213,6 +215,10 @@ struct rbf_plan {
   int* flow_dep_off = nullptr;
   int* flow_dep = nullptr;
   double* u_init = nullptr;        // start field kept for the exact re-run after a failure
+  // two steps per launch (pair_kernels.cu): fixed-step runs of TMA plans
+  rbf::PairPlan pair;
+  bool pair_ok = false;
+  cudaGraphExec_t pair_graph = nullptr;
   int kernel_n = 0;
   bool resident = false;
   size_t resident_smem = 0;
@@ -380,6 +386,24 @@ int launch_step(rbf_plan* p, int in, int flags) {
   return RBF_OK;
 }
 
+// Two steps in one launch (pair_kernels.cu): U[in] -> U[1-in].
+int launch_pair(rbf_plan* p, int in, int flags) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p->pair.grid);
+  cfg.blockDim = dim3(p->pair.block);
+  cfg.dynamicSmemBytes = p->pair.smem;
+  cfg.stream = p->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = p->pdl ? 1 : 0;
+  RBF_CK(cudaLaunchKernelEx(&cfg, p->pair.fn, p->pair.args, static_cast<const double*>(p->U[in]),
+                            p->U[1 - in], flags, p->pair.geom));
+  ++p->launches;
+  return RBF_OK;
+}
+
 // A copy-back step (paper Listing 1, solver.py:213): U[0] -> U[1], then U[0] = U[1].
 int launch_copy_back_step(rbf_plan* p, int flags) {
   RBF_TRY(launch_step(p, 0, flags));
@@ -512,6 +536,54 @@ int run_streaming(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
   cudaEventDestroy(evs[0]);
   cudaEventDestroy(evs[1]);
   return rc;
+}
+
+// Fixed-step loop two steps per launch (pair_kernels.cu), CUDA graphs of
+// kGraphSteps/2 launches, an odd last step on the single-step kernel.  The
+// start field is kept; if any step produced a non-finite value the caller
+// replays the run on the single-step path, which stops at the exact step
+// (*fallback = true).  *final_buf = buffer holding the result.
+int run_pair(rbf_plan* p, int64_t limit, bool* fallback, int* final_buf) {
+  *fallback = false;
+  if (!p->u_init) RBF_CK(cudaMallocAsync(reinterpret_cast<void**>(&p->u_init), sizeof(double) * p->N, p->stream));
+  RBF_CK(cudaMemcpyAsync(p->u_init, p->U[0], sizeof(double) * p->N, cudaMemcpyDeviceToDevice, p->stream));
+  const int64_t pairs = limit / 2;
+  const bool odd = (limit & 1) != 0;
+  constexpr int kPairGraph = kGraphSteps / 2;
+  if (pairs > kPairGraph && !p->pair_graph) {
+    RBF_CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+    const int64_t before = p->launches;
+    int rc = RBF_OK;
+    for (int i = 0; i < kPairGraph && rc == RBF_OK; ++i) rc = launch_pair(p, i & 1, 0);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(p->stream, &g);
+    p->launches = before;
+    if (rc != RBF_OK) return rc;
+    if (e != cudaSuccess) return fail(RBF_ERR_CUDA, std::string("pair graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&p->pair_graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(RBF_ERR_CUDA, std::string("pair graph instantiate: ") + cudaGetErrorString(e));
+  }
+  RBF_CK(cudaEventRecord(p->ev0, p->stream));
+  int64_t done = 0;
+  const int64_t graphed = pairs > kPairGraph ? ((pairs - 1) / kPairGraph) * kPairGraph : 0;
+  for (; done < graphed; done += kPairGraph) {
+    RBF_CK(cudaGraphLaunch(p->pair_graph, p->stream));
+    p->launches += kPairGraph;
+  }
+  for (; done < pairs; ++done)
+    RBF_TRY(launch_pair(p, static_cast<int>(done & 1), (!odd && done == pairs - 1) ? rbf::kNeedResidual : 0));
+  if (odd) RBF_TRY(launch_step(p, static_cast<int>(pairs & 1), rbf::kNeedResidual));
+  RBF_CK(cudaEventRecord(p->ev1, p->stream));
+  *final_buf = static_cast<int>((pairs + (odd ? 1 : 0)) & 1);
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  RBF_TRY(read_status(p));
+  if (p->h_st->bad_step >= 0) {
+    RBF_CK(cudaMemcpyAsync(p->U[0], p->u_init, sizeof(double) * p->N, cudaMemcpyDeviceToDevice, p->stream));
+    RBF_CK(cudaMemcpyAsync(p->U[1], p->u_init, sizeof(double) * p->N, cudaMemcpyDeviceToDevice, p->stream));
+    *fallback = true;
+  }
+  return RBF_OK;
 }
 
 // Fixed-step loop in one persistent launch (flow_kernels.cuh).  Returns
@@ -840,6 +912,31 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
       p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(chunks, int64_t(sms) * std::max(occ, 1))));
       if (!p->resident && !p->cluster_fn) p->variant = 2;
     } else {
+      cudaGetLastError();
+    }
+  }
+  // two-step tile kernel for fixed-step runs (pair_kernels.cu)
+  // Measured (profiles/README.md, tools/pair_sweep.py): 1.1-1.5x faster up to
+  // ~1e6 stencil entries, where the per-launch grid dependency dominates;
+  // even or slower above, where both are bound by the streamed bytes and the
+  // pair kernel's extra phase-2 work.  RBF_PAIR / RBFFD_PAIR=1 force it on.
+  const char* pair_env = std::getenv("RBFFD_PAIR");
+  const bool pair_force = (flags & RBF_PAIR) || (pair_env && std::atoi(pair_env) == 1);
+  const bool pair_off = (flags & RBF_NO_PAIR) || (pair_env && std::atoi(pair_env) == 0);
+  const bool pair_auto = N_i * static_cast<int64_t>(n) <= kPairAutoEntries;
+  if (p->tma_fn && p->index_bits == 16 && !pair_off && (pair_force || pair_auto)) {
+    int tpc = 4;
+    if (const char* e = std::getenv("RBFFD_PAIR_TILES")) tpc = std::max(1, std::atoi(e));
+    int optin = 0;
+    RBF_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    bool ok = false;
+    RBF_TRY(rbf::pair_build(p->args(), p->tma_geom.sps, tpc, sms, static_cast<size_t>(optin) - 2048,
+                            p->stream, &p->pair, &ok));
+    if (ok && set_max_smem(p->pair.fn) == cudaSuccess) {
+      p->pair_ok = true;
+      p->device_bytes += p->pair.halo_slices * 32LL * (12LL * n + 12) + p->S * 32LL * n * 2;
+    } else {
+      if (ok) rbf::pair_free(&p->pair, p->stream);
       cudaGetLastError();
     }
   }
@@ -1571,9 +1668,24 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
   RBF_TRY(normalise_current(p));
   RBF_TRY(reset_status(p, dt, tol));
   int rc;
+  int pair_buf = -1;  // >= 0: the pair path ran and left the field in U[pair_buf]
   PhaseTimer timer;
   if (p->resident) {
     rc = run_resident(p, limit, steady, copy_back != 0);
+  } else if (p->pair_ok && !p->flow_fn && !steady && limit >= 2) {
+    bool fallback = false;
+    int final_buf = 0;
+    rc = run_pair(p, limit, &fallback, &final_buf);
+    if (rc == RBF_OK && fallback) {
+      RBF_TRY(reset_status(p, dt, tol));
+      rc = run_streaming(p, limit, steady, copy_back != 0);
+    } else if (rc == RBF_OK) {
+      pair_buf = final_buf;
+      if (copy_back && final_buf != 0) {  // copy-back runs end with the field in U[0]
+        RBF_CK(cudaMemcpyAsync(p->U[0], p->U[1], sizeof(double) * p->N, cudaMemcpyDeviceToDevice, p->stream));
+        pair_buf = 0;
+      }
+    }
   } else if (p->flow_fn && !steady && !copy_back && limit >= 2) {
     bool fallback = false;
     rc = run_flow(p, limit, &fallback);
@@ -1617,6 +1729,7 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
     return fail(RBF_ERR_INSTABILITY, "time loop unstable at step " + std::to_string(s.bad_step));
   }
   p->cur = (copy_back || p->resident) ? 0 : static_cast<int>(done & 1);
+  if (pair_buf >= 0) p->cur = pair_buf;
   if (steps_done) *steps_done = done;
   if (residual) *residual = have_res ? res : 0.0;
   if (has_residual) *has_residual = have_res ? 1 : 0;
@@ -1688,6 +1801,9 @@ int rbf_plan_get_info(const rbf_plan* p, rbf_plan_info* info) {
   info->flow_grid = p->flow_grid;
   // bytes the streaming step actually moves: 16-bit ids, the per-slice window
   // bases, and int32 ids of the overflow slices
+  info->pair = p->pair_ok ? 1 : 0;
+  info->pair_tiles = p->pair_ok ? p->pair.args.n_tiles : 0;
+  info->pair_halo_rows = p->pair_ok ? p->pair.halo_entries : 0;
   info->stream_bytes_per_step = (p->index_bits == 16 && !p->resident)
       ? p->N_i * (10LL * p->n + 24) + p->S * 16 + p->overflow_slices * 32LL * p->n * 4
       : info->bytes_per_step;
@@ -1716,7 +1832,9 @@ void rbf_plan_destroy(rbf_plan* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   for (auto& g : p->graphs)
     if (g) cudaGraphExecDestroy(g);
+  if (p->pair_graph) cudaGraphExecDestroy(p->pair_graph);
   cudaStream_t s = p->stream;
+  if (p->pair_ok) rbf::pair_free(&p->pair, s);
   pool_free(p->W, s);
   pool_free(p->C, s);
   pool_free(p->F, s);

@@ -141,6 +141,13 @@ def _as(a, dtype) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a), dtype=dtype)
 
 
+def _pair_flags(pair: Optional[bool]) -> int:
+    """None: the library's size rule; True: force the two-step kernel; False: off."""
+    if pair is None:
+        return 0
+    return _lib.RBF_PAIR if pair else _lib.RBF_NO_PAIR
+
+
 def _ptr(a: Optional[np.ndarray]):
     return None if a is None else ctypes.c_void_p(a.ctypes.data)
 
@@ -155,7 +162,7 @@ class Plan:
     def __init__(self, n_total, interior, rows, weights, f_int, positions=None, *,
                  renumber: bool = False, device: int = 0, resident: bool = True,
                  pdl: bool = True, tma: bool = True, cluster: bool = True, idx16: bool = True,
-                 flow: bool = False):
+                 flow: bool = False, pair: Optional[bool] = None):
         self._lib = _lib.load()
         interior = _as(interior, np.int64)
         weights = _as(weights, np.float64)
@@ -185,6 +192,7 @@ class Plan:
             flags |= _lib.RBF_NO_IDX16
         if flow:
             flags |= _lib.RBF_FLOW
+        flags |= _pair_flags(pair)
         handle = ctypes.c_void_p()
         rc = self._lib.rbf_plan_create(
             ctypes.byref(handle), int(n_total), int(n_rows), int(n), _ptr(interior), _ptr(rows),
@@ -200,7 +208,7 @@ class Plan:
     @classmethod
     def assembled(cls, n_total, interior, rows, positions, f_int, degree: int, *,
                   renumber: bool = False, device: int = 0, resident: bool = True,
-                  pdl: bool = True, tma: bool = True) -> "Plan":
+                  pdl: bool = True, tma: bool = True, pair: Optional[bool] = None) -> "Plan":
         """Plan whose weights are assembled on the device (rbf_plan_create_assembled):
         the PHS+monomial solves of weights.py:218-259 run on the GPU straight into
         the SELL layout; the host never holds the weights."""
@@ -212,7 +220,8 @@ class Plan:
         pos = _as(positions, np.float64)
         n_rows, n = rows.shape
         flags = (_lib.RBF_RENUMBER_MORTON if renumber else 0) | (0 if resident else _lib.RBF_NO_RESIDENT) \
-            | (0 if pdl else _lib.RBF_NO_PDL) | (0 if tma else _lib.RBF_STREAM_LDG)
+            | (0 if pdl else _lib.RBF_NO_PDL) | (0 if tma else _lib.RBF_STREAM_LDG) \
+            | _pair_flags(pair)
         handle = ctypes.c_void_p()
         rc = self._lib.rbf_plan_create_assembled(
             ctypes.byref(handle), int(n_total), int(n_rows), int(n), int(degree), _ptr(interior),
@@ -229,7 +238,8 @@ class Plan:
 
     @classmethod
     def load(cls, path, *, device: int = 0, resident: bool = True, pdl: bool = True,
-             tma: bool = True, cluster: bool = True, idx16: bool = True) -> "Plan":
+             tma: bool = True, cluster: bool = True, idx16: bool = True,
+             pair: Optional[bool] = None) -> "Plan":
         """Load a plan written by ``save`` straight into HBM (rbf_plan_load)."""
         import numpy as _np  # noqa: F401
 
@@ -237,7 +247,7 @@ class Plan:
         self._lib = _lib.load()
         flags = (0 if resident else _lib.RBF_NO_RESIDENT) | (0 if pdl else _lib.RBF_NO_PDL) \
             | (0 if tma else _lib.RBF_STREAM_LDG) | (0 if cluster else _lib.RBF_NO_CLUSTER) \
-            | (0 if idx16 else _lib.RBF_NO_IDX16)
+            | (0 if idx16 else _lib.RBF_NO_IDX16) | _pair_flags(pair)
         handle = ctypes.c_void_p()
         self._check(self._lib.rbf_plan_load(ctypes.byref(handle), str(path).encode(), int(device), flags))
         self._h = handle

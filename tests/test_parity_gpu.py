@@ -409,6 +409,70 @@ def test_flow_loop_step_counts(synth_cache, steps):
         plan.close()
 
 
+# ---- two steps per launch (pair_kernels.cu) ---------------------------------
+@pytest.mark.parametrize("target,n,m", [(20_000, 15, 2), (20_000, 30, 4), (200_000, 15, 2), (50_000, 12, 2)])
+@pytest.mark.parametrize("renumber", [False, True], ids=["native", "morton"])
+def test_pair_kernel_matches_oracle(synth_cache, target, n, m, renumber):
+    """Tile-local temporal blocking: every step count (pairs, an odd last
+    step, graph-chunked runs), swap and copy-back, bitwise vs the oracle."""
+    nodes, _, shapes = _synth(synth_cache, target, n, m)
+    interior = shapes.interior_nodes
+    plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                rb.forcing(nodes.positions[interior]), nodes.positions, renumber=renumber, pair=True)
+    info = plan.info()
+    assert info["pair"] == 1 and info["pair_tiles"] > 0 and info["pair_halo_rows"] > 0
+    u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    dt = 0.5 * rb.stability_bound(shapes)
+    for steps in (1, 2, 3, 64, 65, 130, 131):
+        want = orc.run_time_loop(nodes, shapes, steps=steps)
+        for copy_back in (False, True):
+            plan.set_field(u0)
+            res = plan.run(dt, steps=steps, copy_back=copy_back)
+            assert res.steps_done == steps and res.residual == want["residual"], (steps, copy_back)
+            assert np.array_equal(plan.get_field(), want["field"]), (steps, copy_back)
+    # a run continuing from the previous field (the plan tracks the buffer)
+    plan.set_field(u0)
+    plan.run(dt, steps=33)
+    plan.run(dt, steps=40)
+    want = orc.run_time_loop(nodes, shapes, steps=73)
+    assert np.array_equal(plan.get_field(), want["field"])
+    plan.close()
+
+
+def test_pair_kernel_off_and_auto(synth_cache):
+    nodes, _, shapes = _synth(synth_cache, 20_000, 15, 2)
+    interior = shapes.interior_nodes
+    args = (nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+            rb.forcing(nodes.positions[interior]), nodes.positions)
+    assert Plan(*args, renumber=True).info()["pair"] == 1          # small: on by default
+    assert Plan(*args, renumber=True, pair=False).info()["pair"] == 0
+    nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
+    interior = shapes.interior_nodes
+    big = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+               rb.forcing(nodes.positions[interior]), nodes.positions, renumber=True)
+    assert big.info()["pair"] == 0                                  # N_i*n > 1e6: single step
+
+
+def test_pair_kernel_failure_replays_the_exact_step(synth_cache):
+    """A non-finite value inside a pair is replayed on the single-step path:
+    the failing step and field are the reference's (solver.py:200-206)."""
+    nodes, _, shapes = _synth(synth_cache, 20_000, 15, 2)
+    interior = shapes.interior_nodes
+    plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                rb.forcing(nodes.positions[interior]), nodes.positions, renumber=True, pair=True)
+    dt = 40.0 * rb.stability_bound(shapes)
+    want = orc.run_time_loop(nodes, shapes, dt=dt, steps=400)
+    assert want["status"] == orc.ORC_INSTABILITY
+    plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
+    res = plan.run(dt, steps=400)
+    assert res.status == _lib.RBF_ERR_INSTABILITY and res.bad_step == want["step"]
+    assert np.array_equal(plan.get_field(), want["field"], equal_nan=True)
+    plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
+    res = plan.run(0.5 * rb.stability_bound(shapes), steps=77)
+    want = orc.run_time_loop(nodes, shapes, steps=77)
+    assert np.array_equal(plan.get_field(), want["field"]) and res.residual == want["residual"]
+
+
 def test_idx16_overflow_slices_path(synth_cache, monkeypatch):
     """Force 16-bit ids on the native (non-Morton) order, where many slices
     overflow the two windows and read int32 ids from HBM instead."""
