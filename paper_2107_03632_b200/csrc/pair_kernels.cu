@@ -21,11 +21,20 @@
 // ids), the 2n bytes of local ids and one field write.
 //
 // Pipeline: the TMA ring of step_tma_kernel (one producer lane, CW consumer
-// warps, cp.async.bulk + mbarrier transaction counts), streaming per tile the
-// chunk sequence [phase-1 main | phase-1 halo | phase-2 main]; consumer warps
-// meet at one named barrier per tile between the phases, the producer keeps
-// streaming through it.  U1 is double-buffered so the next tile's phase 1
-// never waits for the current tile's phase 2.
+// warps, cp.async.bulk + mbarrier transaction counts) streams phase-1 data
+// only, per tile [main rows | halo rows]; the producer also prefetches each
+// tile's local ids into L2.  Consumers walk segments: segment k interleaves
+// phase 1 of tile k (ring) with phase 2 of tile k-1 (direct loads of the
+// L2-resident weights/forcing and the prefetched local ids), so HBM streams
+// the next tile while the previous one finishes; the consumer warps meet at
+// one named barrier per segment, and U1 is double-buffered (tile k writes
+// buffer k&1 while tile k-1 is read from the other).
+//
+// Measured (profiles/README.md): HBM traffic per pair is as designed (268 MB
+// read at C2 against 2 x 172 MB for two single steps), but the consumers are
+// latency-bound (15 warps, ~2 us per 32-row unit), so the pair only wins
+// where the per-launch grid dependency dominates -- 1.1-1.5x up to ~1e6
+// stencil entries -- and the driver enables it there by default.
 //
 // Failure semantics: the epilogue flags a non-finite value anywhere in the
 // pair and the driver replays the run on the single-step path, which stops at
