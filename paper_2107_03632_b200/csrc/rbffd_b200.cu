@@ -362,6 +362,56 @@ int staging_acquire(Staging& sg, int device) {
 }
 
 
+// Field transfers through the pinned staging pair: pageable copies of a
+// whole field run at a fraction of the link rate (the driver stages them
+// through its own small bounce buffers); here the DMA of chunk c overlaps the
+// host copy of chunk c-1, and the host copies use every core.
+constexpr size_t kFieldStagedMin = size_t(4) << 20;  // bytes; below this a plain copy is faster
+
+int staged_d2h(double* dst, const double* dsrc, size_t count, cudaStream_t st, int device) {
+  Staging& sg = staging();
+  std::lock_guard<std::mutex> lk(sg.mu);
+  RBF_TRY(staging_acquire(sg, device));
+  const size_t chunk = sg.cap / sizeof(double);
+  const size_t nchunks = (count + chunk - 1) / chunk;
+  for (size_t c = 0; c <= nchunks; ++c) {
+    if (c < nchunks) {  // start the DMA of chunk c
+      const int b = static_cast<int>(c & 1);
+      const size_t lo = c * chunk, n = std::min(chunk, count - lo);
+      RBF_CK(cudaMemcpyAsync(sg.buf[b], dsrc + lo, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      RBF_CK(cudaEventRecord(sg.ev[b], st));
+    }
+    if (c > 0) {  // drain chunk c-1 into the caller's buffer
+      const int b = static_cast<int>((c - 1) & 1);
+      const size_t lo = (c - 1) * chunk, n = std::min(chunk, count - lo);
+      RBF_CK(cudaEventSynchronize(sg.ev[b]));
+      const double* src = reinterpret_cast<const double*>(sg.buf[b]);
+#pragma omp parallel for schedule(static)
+      for (int64_t e = 0; e < static_cast<int64_t>(n); ++e) dst[lo + e] = src[e];
+    }
+  }
+  return RBF_OK;
+}
+
+int staged_h2d(double* ddst, const double* src, size_t count, cudaStream_t st, int device) {
+  Staging& sg = staging();
+  std::lock_guard<std::mutex> lk(sg.mu);
+  RBF_TRY(staging_acquire(sg, device));
+  const size_t chunk = sg.cap / sizeof(double);
+  for (size_t lo = 0, c = 0; lo < count; lo += chunk, ++c) {
+    const int b = static_cast<int>(c & 1);
+    const size_t n = std::min(chunk, count - lo);
+    RBF_CK(cudaEventSynchronize(sg.ev[b]));  // the previous DMA out of this buffer is done
+    double* hb = reinterpret_cast<double*>(sg.buf[b]);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < static_cast<int64_t>(n); ++e) hb[e] = src[lo + e];
+    RBF_CK(cudaMemcpyAsync(ddst + lo, hb, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    RBF_CK(cudaEventRecord(sg.ev[b], st));
+  }
+  RBF_CK(cudaStreamSynchronize(st));
+  return RBF_OK;
+}
+
 // One streaming step: reads U[in], writes U[1-in].
 int launch_step(rbf_plan* p, int in, int flags) {
   if (p->N_i == 0) return RBF_OK;
@@ -1626,11 +1676,14 @@ int rbf_set_field(rbf_plan* p, const double* u) {
   if (!p || !u) return fail(RBF_ERR_PARAM, "NULL argument");
   RBF_CK(cudaSetDevice(p->device));
   const size_t bytes = sizeof(double) * p->N;
+  const bool staged = bytes >= kFieldStagedMin;
   if (!p->new_id) {
-    RBF_CK(cudaMemcpyAsync(p->U[0], u, bytes, cudaMemcpyHostToDevice, p->stream));
+    if (staged) RBF_TRY(staged_h2d(p->U[0], u, static_cast<size_t>(p->N), p->stream, p->device));
+    else RBF_CK(cudaMemcpyAsync(p->U[0], u, bytes, cudaMemcpyHostToDevice, p->stream));
     RBF_CK(cudaMemcpyAsync(p->U[1], p->U[0], bytes, cudaMemcpyDeviceToDevice, p->stream));
   } else {
-    RBF_CK(cudaMemcpyAsync(p->tmp, u, bytes, cudaMemcpyHostToDevice, p->stream));
+    if (staged) RBF_TRY(staged_h2d(p->tmp, u, static_cast<size_t>(p->N), p->stream, p->device));
+    else RBF_CK(cudaMemcpyAsync(p->tmp, u, bytes, cudaMemcpyHostToDevice, p->stream));
     const int blocks = static_cast<int>(std::min<int64_t>((p->N + 255) / 256, 148 * 16));
     rbf::scatter_field_kernel<<<blocks, 256, 0, p->stream>>>(p->tmp, p->new_id, p->N, p->U[0], p->U[1]);
     RBF_CK(cudaGetLastError());
@@ -1644,14 +1697,15 @@ int rbf_get_field(rbf_plan* p, double* u) {
   if (!p || !u) return fail(RBF_ERR_PARAM, "NULL argument");
   RBF_CK(cudaSetDevice(p->device));
   const size_t bytes = sizeof(double) * p->N;
-  if (!p->new_id) {
-    RBF_CK(cudaMemcpyAsync(u, p->U[p->cur], bytes, cudaMemcpyDeviceToHost, p->stream));
-  } else {
+  const double* src = p->U[p->cur];
+  if (p->new_id) {
     const int blocks = static_cast<int>(std::min<int64_t>((p->N + 255) / 256, 148 * 16));
     rbf::gather_field_kernel<<<blocks, 256, 0, p->stream>>>(p->U[p->cur], p->new_id, p->N, p->tmp);
     RBF_CK(cudaGetLastError());
-    RBF_CK(cudaMemcpyAsync(u, p->tmp, bytes, cudaMemcpyDeviceToHost, p->stream));
+    src = p->tmp;
   }
+  if (bytes >= kFieldStagedMin) return staged_d2h(u, src, static_cast<size_t>(p->N), p->stream, p->device);
+  RBF_CK(cudaMemcpyAsync(u, src, bytes, cudaMemcpyDeviceToHost, p->stream));
   RBF_CK(cudaStreamSynchronize(p->stream));
   return RBF_OK;
 }

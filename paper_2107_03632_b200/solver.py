@@ -29,7 +29,7 @@ from typing import Optional
 
 import numpy as np
 
-from . import _lib
+from . import _lib, _par
 from .errors import DeviceError, InstabilityError, ParameterError, SteadyStateTimeout
 from .problem import closed_form_solution, forcing, monomial_count, spacing_for_node_count
 
@@ -450,7 +450,7 @@ def run_time_loop(config: SolveConfig, nodes, shapes, copy_back: bool = False, *
     # the Dirichlet values (solver.py:130-138) and the error norms
     # (solver.py:239-246): elementwise, so each use gets the reference's bits
     exact = closed_form_solution(nodes.positions)
-    f_int = np.ascontiguousarray(2.0 * np.pi**2 * exact[interior])  # solver.py:184
+    f_int = _par.scaled_gather(2.0 * np.pi**2, exact, np.asarray(interior))  # solver.py:184
     u1 = np.zeros(nodes.n_total)  # solver.py:186
     bidx = nodes.boundary_indices
     u1[bidx] = exact[bidx]
@@ -515,18 +515,15 @@ class _Ticker:
 
 
 def _norms(values: np.ndarray, exact: np.ndarray):
-    diff = np.asarray(values, dtype=float) - exact
-    return float(np.max(np.abs(diff))), float(math.sqrt(float((diff**2).mean())))
+    # max|u-u*| and sqrt(mean((u-u*)**2)) on all cores, numpy's bits (_par.py)
+    return _par.error_norms(values, exact)
 
 
 def error_norms(values: np.ndarray, nodes):
     """(linf, l2) of values minus the analytic solution over all nodes (solver.py:239-246)."""
     if len(values) != nodes.n_total:
         raise ParameterError("field length does not match the node set")
-    diff = np.asarray(values, dtype=float) - closed_form_solution(nodes.positions)
-    linf = float(np.max(np.abs(diff)))
-    l2 = float(math.sqrt(float((diff**2).mean())))
-    return linf, l2
+    return _par.error_norms(values, closed_form_solution(nodes.positions))
 
 
 def stability_bound(shapes) -> float:

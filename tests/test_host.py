@@ -137,3 +137,22 @@ def test_problem_cache_round_trip(tmp_path, golden):
     # host prep is unchanged on memory-mapped arrays
     assert rb.stability_bound(sh2) == rb.stability_bound(shapes)
     assert np.array_equal(rb.forcing(n2.positions), rb.forcing(nodes.positions))
+
+
+def test_parallel_host_reductions_have_numpy_bits():
+    """_par: the chunked / tree-split versions of the host pieces of the solve
+    path (forcing gather, error norms) equal numpy's single calls bit for bit."""
+    import math
+
+    from paper_2107_03632_b200 import _par
+
+    rng = np.random.default_rng(7)
+    for n in (17, 1000, 300_001, 2_000_003):
+        v = rng.standard_normal(n)
+        e = rng.standard_normal(n) * 0.25
+        diff = v - e
+        assert _par.error_norms(v, e) == (float(np.max(np.abs(diff))), math.sqrt(float((diff ** 2).mean())))
+        x = rng.random(n) ** 2
+        assert _par.pairwise_sum(x) == float(np.add.reduce(x))
+        idx = rng.integers(0, n, n // 2 + 1)
+        assert np.array_equal(_par.scaled_gather(2.0 * np.pi**2, x, idx), 2.0 * np.pi**2 * x[idx])
