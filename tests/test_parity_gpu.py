@@ -409,6 +409,52 @@ def test_flow_loop_step_counts(synth_cache, steps):
         plan.close()
 
 
+# ---- every specialised stencil width (and two generic ones) -----------------
+WIDTHS = [4, 5, 6, 7, 8, 9, 10, 11, 12, 15, 16, 20, 21, 24, 28, 30, 32, 33, 36, 40, 42, 45, 48, 56, 60, 64]
+SPECIALISED = {4, 5, 6, 7, 8, 9, 10, 12, 15, 16, 20, 21, 24, 28, 30, 32, 36, 40, 42, 45, 48, 56, 60, 64}
+
+
+def _degree_for(n):
+    return 1 if n < 12 else (2 if n < 30 else (4 if n < 56 else 6))
+
+
+@pytest.mark.parametrize("n", WIDTHS)
+def test_every_width_matches_oracle(n):
+    """All kernel instantiations (single-step TMA ring with 16-bit / int32 ids,
+    plain-load streaming, two-step tile kernel, generic runtime-n loop) on a
+    scattered disk at each width, bitwise vs the oracle."""
+    m = _degree_for(n)
+    nodes, st, shapes = synth.synthetic_problem(12_000, n, m, seed=5, weights="gpu")
+    interior = shapes.interior_nodes
+    rows = st.neighbors[interior]
+    f_int = rb.forcing(nodes.positions[interior])
+    u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    dt = 0.5 * rb.stability_bound(shapes)
+    steps = 24
+    want = orc.run_time_loop(nodes, shapes, steps=steps)
+    stream = dict(resident=False, cluster=False)
+    variants = [  # (plan flags, expected variant, expected pair)
+        (dict(renumber=True), None, None),                                  # default choice
+        (dict(renumber=True, pair=False, **stream), 2, 0),                  # TMA ring, 16-bit ids (n <= 32)
+        (dict(renumber=True, pair=True, **stream), 2, 1 if n <= 32 and n in SPECIALISED else 0),
+        (dict(renumber=True, idx16=False, pair=False, **stream), 2, 0),     # TMA ring, int32 ids
+        (dict(renumber=False, tma=False, pair=False, **stream), 1, 0),      # plain-load streaming
+        (dict(renumber=True, cluster=False), None, None),                   # single-CTA resident loop
+    ]
+    for kw, variant, pair in variants:
+        plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, nodes.positions, **kw)
+        info = plan.info()
+        if variant is not None and n in SPECIALISED:
+            assert info["variant"] == variant, (n, kw, info)
+        if pair is not None:
+            assert info["pair"] == pair, (n, kw, info)
+        plan.set_field(u0)
+        res = plan.run(dt, steps=steps)
+        assert res.residual == want["residual"], (n, kw)
+        assert np.array_equal(plan.get_field(), want["field"]), (n, kw)
+        plan.close()
+
+
 # ---- two steps per launch (pair_kernels.cu) ---------------------------------
 @pytest.mark.parametrize("target,n,m", [(20_000, 15, 2), (20_000, 30, 4), (200_000, 15, 2), (50_000, 12, 2)])
 @pytest.mark.parametrize("renumber", [False, True], ids=["native", "morton"])
