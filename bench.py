@@ -201,7 +201,7 @@ def run_reference(args, workload):
         "metric": METRIC,
         "value": rate,
         "unit": "node-updates/s",
-        "n_gpus": 0,
+        "n_gpus": args.gpus,  # the configuration's; this arm itself runs on the host cores
         "steps": steps,
         "warmup": args.warmup,
         "ms_per_step": 1e3 * out["seconds"] / steps,
@@ -209,8 +209,8 @@ def run_reference(args, workload):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": ("synthetic (reference advancing-front nodes via the native generator, GPU kNN + weights)"
-                 if workload != "c1" else "reference fixture (tests/golden/dome.npz)"),
+        "data": ("synthetic (reference advancing-front nodes via the native generator, CPU kNN "
+                 "(cKDTree) + numpy/LAPACK weights)" if workload != "c1" else "reference fixture (tests/golden/dome.npz)"),
         "config": {"workload": WORKLOADS[workload][3], "N": int(nodes.n_total),
                    "N_i": int(interior.size), "n": int(shapes.weights.shape[1]),
                    "m": int(shapes.degree), "dt": dt},
@@ -344,8 +344,8 @@ def main():
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": ("synthetic (reference advancing-front nodes via the native generator)"
-                 if args.workload != "c1" else "reference fixture"),
+        "data": ("synthetic (reference advancing-front nodes via the native generator, GPU kNN + "
+                 "GPU-assembled weights)" if args.workload != "c1" else "reference fixture"),
         "config": {
             "workload": WORKLOADS[args.workload][3],
             "N": int(nodes.n_total), "N_i": N_i, "n": n, "m": int(shapes.degree), "dt": dt,
