@@ -254,6 +254,28 @@ int rbf_group_run(rbf_group* group, double dt, int64_t steps, int32_t mode, doub
                   int32_t* has_residual, int64_t* bad_step, double* device_seconds);
 void rbf_group_destroy(rbf_group* group);
 
+/*
+ * Push-mode halo exchange for fixed-step runs (BASELINE.json north star (4),
+ * "NCCL or P2P"; replaces pack + NCCL send/recv): after each step a small
+ * kernel stores the owned values the neighbours read straight into their field
+ * buffers (P2P stores over NVLink, CUDA IPC mappings between processes) and
+ * publishes the arrival with a system-scope release store; the next step's
+ * consumers wait (acquire) for their neighbours' arrivals.  Bitwise identical
+ * to the NCCL path.  Steady-mode runs and failure replays keep the exact
+ * per-step NCCL / copy path.
+ *   rbf_group_push_local   parts of one process (one device): plain pointers
+ *   rbf_group_push_export  one part per process: the blob (<= 1024 bytes) its
+ *                          peers need -- IPC handles of its field buffers and
+ *                          arrival counters, its halo slices per owner
+ *   rbf_group_push_import  all ranks' blobs, `stride` bytes apart; every rank
+ *                          must import before any rank runs (hold a barrier)
+ *   rbf_group_push_mode    1 when the group's fast path pushes
+ */
+int rbf_group_push_local(rbf_group* group);
+int rbf_group_push_export(rbf_group* group, void* blob_out, int64_t capacity, int64_t* length);
+int rbf_group_push_import(rbf_group* group, int32_t n_blobs, const void* blobs, int64_t stride);
+int rbf_group_push_mode(const rbf_group* group);
+
 void rbf_plan_destroy(rbf_plan* plan);
 const char* rbf_last_error(void);
 int rbf_version(void);

@@ -61,7 +61,14 @@ def main(args, metric, workloads):  # pragma: no cover - needs >1 GPU
     t_setup = time.perf_counter() - t0
     uid = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
-    group = NcclGroup(me, rank, world, local, uid[0])
+    def allgather(blob: bytes):
+        out = [None] * world
+        dist.all_gather_object(out, blob)
+        return out
+
+    push = os.environ.get("RBFFD_GROUP_PUSH", "1") != "0"
+    group = NcclGroup(me, rank, world, local, uid[0], allgather=allgather if push else None)
+    dist.barrier()  # every rank mapped its neighbours before any rank pushes
     plan = group.plans[0]
     u0 = apply_dirichlet(nodes, np.zeros(nodes.n_total))
     u_loc = me.local_field(u0)
@@ -103,7 +110,9 @@ def main(args, metric, workloads):  # pragma: no cover - needs >1 GPU
             "data": "synthetic",
             "config": {"workload": f"{desc} per GPU (weak scaling, one disk of {nodes.n_total} nodes)",
                        "N": int(nodes.n_total), "N_i": n_rows_total, "n": n, "m": m, "dt": dt,
-                       "parallelism": f"node-partitioned x{world}, NCCL halo exchange",
+                       "parallelism": (f"node-partitioned x{world}, halo exchange: "
+                                       + ("P2P push over NVLink (CUDA IPC), fused arrival flags"
+                                          if group.push_mode else "NCCL send/recv")),
                        "halo_bytes_per_step_rank0": me.halo_bytes_per_step(),
                        "setup_seconds": t_setup},
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s per GPU",
@@ -111,7 +120,7 @@ def main(args, metric, workloads):  # pragma: no cover - needs >1 GPU
             "e2e": {"value": args.steps * n_rows_total / te.item(), "unit": "node-updates/s",
                     "h2d_bytes_per_step": 8 * nodes.n_total / args.steps,
                     "d2h_bytes_per_step": 8 * nodes.n_total / args.steps},
-            "gpu_launches": 4 * args.steps,
+            "gpu_launches": (2 if group.push_mode else 4) * args.steps,
         }
         print(json.dumps(line), flush=True)
     group.close()

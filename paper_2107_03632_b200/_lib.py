@@ -60,6 +60,10 @@ EXPORTED = (
     "rbf_knn",
     "rbf_generate_unit_disk_nodes",
     "rbf_free_host",
+    "rbf_group_push_local",
+    "rbf_group_push_export",
+    "rbf_group_push_import",
+    "rbf_group_push_mode",
 )
 
 
@@ -153,6 +157,10 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "rbf_knn": ([vp, i64, i32, vp, i32], i32),
         "rbf_generate_unit_disk_nodes": ([ctypes.c_double, vp, i32, vp, vp, vp], i32),
         "rbf_free_host": ([vp], None),
+        "rbf_group_push_local": ([vp], i32),
+        "rbf_group_push_export": ([vp, vp, i64, vp], i32),
+        "rbf_group_push_import": ([vp, i32, vp, i64], i32),
+        "rbf_group_push_mode": ([vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -43,6 +43,8 @@ struct DevStatus {
   double dt;
   double tol;
   unsigned long long red[2];         // distributed mode: [residual bits max, non-finite any]
+  long long push_base;               // push-mode groups: arrivals counted before this run
+  long long push_count;              // push-mode groups: halo pushes completed in this run
 };
 
 struct StepArgs {
@@ -55,7 +57,50 @@ struct StepArgs {
   long long dst_base;            // node id of row 0 (= N - N_i)
   int n;
   DevStatus* st;
+  // push-mode partitioned runs (group.inc.cuh): before reading the field, wait
+  // until every neighbour part has pushed the halo of this step into this
+  // part's buffers (wait_flags[id] counts neighbour id's pushes), or null
+  const unsigned long long* wait_flags;
+  unsigned long long wait_mask;  // bit i: part i is a neighbour
 };
+
+constexpr int kMaxPushPeers = 8;
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Push-mode wait: every neighbour's arrival count must reach this part's own
+// push count, i.e. the neighbour finished the previous step (its halo values
+// for this step are in place and it no longer reads the buffer this step
+// writes into its peers).  One lane of the CTA's first consumer warp polls
+// with acquire loads; the other consumer warps are released by a named
+// barrier (nthreads = all consumer threads), which orders their field reads
+// after the acquire.  A wait longer than ~20 s means a peer died: trap
+// instead of hanging the GPU.
+__device__ __forceinline__ void wait_peers(const unsigned long long* flags, unsigned long long mask,
+                                           DevStatus* st, bool first_warp, int nthreads) {
+  if (!flags) return;
+  if (first_warp && (threadIdx.x & 31) == 0) {
+    const unsigned long long need = static_cast<unsigned long long>(
+        *reinterpret_cast<volatile long long*>(&st->push_base) +
+        *reinterpret_cast<volatile long long*>(&st->push_count));
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (unsigned long long m = mask; m; m &= m - 1) {
+      const int j = __ffsll(static_cast<long long>(m)) - 1;
+      while (ld_acquire_sys_u64(flags + j) < need) {
+        __nanosleep(64);
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) __trap();
+      }
+    }
+  }
+  asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+}
 
 enum StepFlags : int {
   kNeedResidual = 1,  // compute max|u2-u1| for this step
@@ -216,7 +261,9 @@ step_stream_kernel(StepArgs a, const double* u_in, double* u_out, int flags) {
   const long long gstep = *reinterpret_cast<volatile long long*>(&st->step);
   const long long bs = *reinterpret_cast<volatile long long*>(&st->bad_step);
   const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
-  if ((bs >= 0 && bs < gstep) || (cs >= 0 && cs < gstep)) return;  // loop already stopped
+  // loop already stopped (push-mode groups keep stepping: the peers wait on us)
+  if (!a.wait_flags && ((bs >= 0 && bs < gstep) || (cs >= 0 && cs < gstep))) return;
+  wait_peers(a.wait_flags, a.wait_mask, a.st, threadIdx.x < 32, static_cast<int>(blockDim.x));
   const double dt = st->dt;
 
   bool bad = false;

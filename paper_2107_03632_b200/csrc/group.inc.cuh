@@ -81,7 +81,25 @@ struct rbf_group {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaGraphExec_t fast_graph = nullptr;  // kGroupGraph fixed-mode steps (pack, exchange, step)
   long long* d_red = nullptr;            // [2] end-of-run reduction: {first bad step key, residual bits}
+  // push mode (fixed-step fast path): halos stored straight into the peers'
+  // buffers by push_halo_kernel, arrivals signalled through per-part counters
+  bool push = false;
+  std::vector<rbf::PushArgs> push_args;  // per local part
+  std::vector<unsigned int*> tickets;
+  std::vector<void*> ipc_opened;         // IPC mappings to close on destroy
 };
+
+// What one part publishes so that its peers can push into it (IPC mode).
+struct PushBlob {
+  int magic;
+  int part_id;
+  cudaIpcMemHandle_t u0, u1, flags;
+  int n_peers;
+  int peer_ids[rbf::kMaxPushPeers];
+  long long recv_off[rbf::kMaxPushPeers];
+  long long recv_count[rbf::kMaxPushPeers];
+};
+constexpr int kPushMagic = 0x52424650;  // "RBFP"
 
 namespace {
 
@@ -148,12 +166,81 @@ int group_reduce_decide(rbf_group* g, int64_t step, int flags) {
   return RBF_OK;
 }
 
+// Field buffers a peer can write into: cudaMalloc'd (pool memory cannot be
+// exported through CUDA IPC), plus the part's arrival counters.  The plan's
+// captured graphs refer to the old buffers and are dropped.
+int push_prepare_part(rbf_plan* p) {
+  if (p->u_legacy) return RBF_OK;
+  RBF_CK(cudaSetDevice(p->device));
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  double* nu[2] = {nullptr, nullptr};
+  for (int b = 0; b < 2; ++b) {
+    RBF_CK(cudaMalloc(&nu[b], sizeof(double) * std::max<int64_t>(p->N, 1)));
+    RBF_CK(cudaMemcpy(nu[b], p->U[b], sizeof(double) * p->N, cudaMemcpyDeviceToDevice));
+    pool_free(p->U[b], p->stream);
+    p->U[b] = nu[b];
+  }
+  RBF_CK(cudaMalloc(&p->push_flags, sizeof(unsigned long long) * 64));
+  RBF_CK(cudaMemset(p->push_flags, 0, sizeof(unsigned long long) * 64));
+  for (auto& gr : p->graphs)
+    if (gr) {
+      cudaGraphExecDestroy(gr);
+      gr = nullptr;
+    }
+  if (p->pair_graph) {
+    cudaGraphExecDestroy(p->pair_graph);
+    p->pair_graph = nullptr;
+  }
+  p->u_legacy = true;
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  return RBF_OK;
+}
+
+int push_finish_part(rbf_group* g, rbf_plan* p, int id, rbf::PushArgs* pa) {
+  if (p->halo_peers.size() > static_cast<size_t>(rbf::kMaxPushPeers))
+    return fail(RBF_ERR_PARAM, "push mode supports at most 8 neighbour parts");
+  if (id < 0 || id >= 64) return fail(RBF_ERR_PARAM, "push mode supports part ids 0..63");
+  pa->u[0] = p->U[0];
+  pa->u[1] = p->U[1];
+  pa->send_idx = p->halo_send_idx;
+  pa->total = p->halo_send_total;
+  pa->my_id = id;
+  pa->st = p->st;
+  unsigned int* ticket = nullptr;
+  RBF_CK(cudaMalloc(&ticket, sizeof(unsigned int)));
+  RBF_CK(cudaMemset(ticket, 0, sizeof(unsigned int)));
+  g->tickets.push_back(ticket);
+  pa->ticket = ticket;
+  p->wait_n = static_cast<int>(p->halo_peers.size());
+  for (int i = 0; i < p->wait_n; ++i) p->wait_ids[i] = p->halo_peers[i];
+  p->push = true;
+  return RBF_OK;
+}
+
+int group_push(rbf_group* g, size_t a, int out) {
+  const rbf::PushArgs& pa = g->push_args[a];
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((pa.total + 255) / 256, 148 * 2)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = g->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RBF_CK(cudaLaunchKernelEx(&cfg, rbf::push_halo_kernel, pa, out));
+  ++g->parts[a]->launches;
+  return RBF_OK;
+}
+
 int group_step_kernel(rbf_group* g, rbf_plan* p, int cur, int flags) {
-  // the plan's own launch path, redirected to the group stream, without PDL
+  // the plan's own launch path, redirected to the group stream (PDL only in
+  // push mode, where the previous kernel of the stream is the push kernel)
   cudaStream_t saved = p->stream;
   const bool pdl = p->pdl;
   p->stream = g->stream;
-  p->pdl = false;
+  p->pdl = pdl && g->push && p->push;
   const int rc = launch_step(p, cur, flags);
   p->stream = saved;
   p->pdl = pdl;
@@ -166,6 +253,13 @@ constexpr int kGroupGraph = 64;  // even: buffer parity is static inside the gra
 // part's step kernel keeps its own first bad step and (on the last step) its
 // residual max in its status, like a single-plan run.
 int group_fast_step(rbf_group* g, int cur, int flags) {
+  if (g->push) {  // step, then push this step's owned halo values into the peers
+    for (size_t a = 0; a < g->parts.size(); ++a) {
+      RBF_TRY(group_step_kernel(g, g->parts[a], cur, flags));
+      RBF_TRY(group_push(g, a, 1 - cur));
+    }
+    return RBF_OK;
+  }
   for (rbf_plan* p : g->parts) RBF_TRY(group_pack(g, p, cur));
   RBF_TRY(group_exchange(g, cur));
   for (rbf_plan* p : g->parts) RBF_TRY(group_step_kernel(g, p, cur, flags));
@@ -210,7 +304,10 @@ int group_run_fast(rbf_group* g, int64_t limit, bool* any_bad, unsigned long lon
   for (int64_t s = chunks * kGroupGraph; s < limit; ++s)
     RBF_TRY(group_fast_step(g, static_cast<int>(s & 1), s == limit - 1 ? rbf::kNeedResidual : 0));
   RBF_CK(cudaEventRecord(g->ev1, g->stream));
-  for (rbf_plan* p : g->parts) p->launches += 2 * limit;
+  for (rbf_plan* p : g->parts) {
+    p->launches += 2 * limit;
+    if (g->push) p->push_base += limit;  // every part ran all `limit` pushes
+  }
   // end-of-run reduction over all parts: min first-bad-step, max residual bits
   if (!g->d_red) RBF_CK(cudaMalloc(&g->d_red, 2 * sizeof(long long)));
   long long key = std::numeric_limits<long long>::max();
@@ -370,6 +467,16 @@ int rbf_group_run(rbf_group* g, double dt, int64_t steps, int32_t mode, double t
       RBF_CK(cudaStreamSynchronize(p->stream));
     }
   }
+  // the exact per-step path exchanges by pack + copy / NCCL: no arrival waits
+  struct PushOff {
+    rbf_group* g;
+    explicit PushOff(rbf_group* gg) : g(gg) {
+      for (rbf_plan* p : g->parts) p->push = false;
+    }
+    ~PushOff() {
+      for (rbf_plan* p : g->parts) p->push = g->push;
+    }
+  } push_off(g);
   RBF_CK(cudaEventRecord(g->ev0, g->stream));
   constexpr int64_t kPoll = 64;
   for (int64_t s = 0; s < limit; ++s) {
@@ -420,10 +527,145 @@ int rbf_group_run(rbf_group* g, double dt, int64_t steps, int32_t mode, double t
   return RBF_OK;
 }
 
+// Push mode for the parts of this process (one device): peers' buffers are
+// plain device pointers.
+int rbf_group_push_local(rbf_group* g) {
+  if (!g) return fail(RBF_ERR_PARAM, "group is NULL");
+  if (g->nccl) return fail(RBF_ERR_PARAM, "use rbf_group_push_export/import for NCCL groups");
+  RBF_CK(cudaSetDevice(g->device));
+  for (rbf_plan* p : g->parts) RBF_TRY(push_prepare_part(p));
+  g->push_args.assign(g->parts.size(), rbf::PushArgs{});
+  for (size_t a = 0; a < g->parts.size(); ++a) {
+    rbf_plan* p = g->parts[a];
+    rbf::PushArgs& pa = g->push_args[a];
+    RBF_TRY(push_finish_part(g, p, g->ids[a], &pa));
+    int np = 0, nn = 0;
+    for (size_t i = 0; i < p->halo_peers.size(); ++i) {
+      auto it = g->local_of.find(p->halo_peers[i]);
+      if (it == g->local_of.end()) return fail(RBF_ERR_PARAM, "peer part not in this group");
+      rbf_plan* q = g->parts[it->second];
+      pa.nbr_flags[nn++] = q->push_flags;
+      if (p->halo_send_count[i] == 0) continue;
+      int j = -1;
+      for (size_t k = 0; k < q->halo_peers.size(); ++k)
+        if (q->halo_peers[k] == g->ids[a]) j = static_cast<int>(k);
+      if (j < 0 || q->halo_recv_count[j] != p->halo_send_count[i])
+        return fail(RBF_ERR_PARAM, "halo lists of two parts disagree");
+      pa.peer[np].u[0] = q->U[0];
+      pa.peer[np].u[1] = q->U[1];
+      pa.peer[np].dst_off = q->halo_recv_off[j];
+      pa.peer[np].src_off = p->halo_send_off[i];
+      pa.peer[np].count = p->halo_send_count[i];
+      ++np;
+    }
+    pa.n_peer = np;
+    pa.n_nbr = nn;
+    pa.sys_scope = 0;  // all parts on this device
+  }
+  if (g->fast_graph) {
+    cudaGraphExecDestroy(g->fast_graph);
+    g->fast_graph = nullptr;
+  }
+  g->push = true;
+  return RBF_OK;
+}
+
+// IPC mode (one part per process): the blob this part publishes.
+int rbf_group_push_export(rbf_group* g, void* out, int64_t cap, int64_t* len) {
+  if (!g || !out || !len) return fail(RBF_ERR_PARAM, "NULL argument");
+  if (g->parts.size() != 1) return fail(RBF_ERR_PARAM, "IPC push mode holds one part per process");
+  if (cap < static_cast<int64_t>(sizeof(PushBlob))) return fail(RBF_ERR_PARAM, "export buffer too small");
+  RBF_CK(cudaSetDevice(g->device));
+  rbf_plan* p = g->parts[0];
+  if (p->halo_peers.size() > static_cast<size_t>(rbf::kMaxPushPeers))
+    return fail(RBF_ERR_PARAM, "push mode supports at most 8 neighbour parts");
+  RBF_TRY(push_prepare_part(p));
+  PushBlob b;
+  std::memset(&b, 0, sizeof(b));
+  b.magic = kPushMagic;
+  b.part_id = g->ids[0];
+  RBF_CK(cudaIpcGetMemHandle(&b.u0, p->U[0]));
+  RBF_CK(cudaIpcGetMemHandle(&b.u1, p->U[1]));
+  RBF_CK(cudaIpcGetMemHandle(&b.flags, p->push_flags));
+  b.n_peers = static_cast<int>(p->halo_peers.size());
+  for (int i = 0; i < b.n_peers; ++i) {
+    b.peer_ids[i] = p->halo_peers[i];
+    b.recv_off[i] = p->halo_recv_off[i];
+    b.recv_count[i] = p->halo_recv_count[i];
+  }
+  std::memcpy(out, &b, sizeof(b));
+  *len = static_cast<int64_t>(sizeof(b));
+  return RBF_OK;
+}
+
+// IPC mode: map the neighbours' buffers from their blobs (all parts' blobs,
+// `stride` bytes apart) and switch the fast path to push mode.  Every rank
+// must import before any rank runs (the caller holds a barrier).
+int rbf_group_push_import(rbf_group* g, int32_t n_blobs, const void* blobs, int64_t stride) {
+  if (!g || !blobs || n_blobs < 1 || stride < static_cast<int64_t>(sizeof(PushBlob)))
+    return fail(RBF_ERR_PARAM, "bad push import arguments");
+  if (g->parts.size() != 1) return fail(RBF_ERR_PARAM, "IPC push mode holds one part per process");
+  RBF_CK(cudaSetDevice(g->device));
+  rbf_plan* p = g->parts[0];
+  RBF_TRY(push_prepare_part(p));
+  std::map<int, PushBlob> by_id;
+  for (int k = 0; k < n_blobs; ++k) {
+    PushBlob b;
+    std::memcpy(&b, static_cast<const unsigned char*>(blobs) + k * stride, sizeof(b));
+    if (b.magic != kPushMagic) return fail(RBF_ERR_PARAM, "not a push-mode blob");
+    by_id[b.part_id] = b;
+  }
+  g->push_args.assign(1, rbf::PushArgs{});
+  rbf::PushArgs& pa = g->push_args[0];
+  RBF_TRY(push_finish_part(g, p, g->ids[0], &pa));
+  int np = 0, nn = 0;
+  for (size_t i = 0; i < p->halo_peers.size(); ++i) {
+    const int q = p->halo_peers[i];
+    auto it = by_id.find(q);
+    if (it == by_id.end()) return fail(RBF_ERR_PARAM, "missing blob of a neighbour part");
+    const PushBlob& b = it->second;
+    void* fl = nullptr;
+    RBF_CK(cudaIpcOpenMemHandle(&fl, b.flags, cudaIpcMemLazyEnablePeerAccess));
+    g->ipc_opened.push_back(fl);
+    pa.nbr_flags[nn++] = static_cast<unsigned long long*>(fl);
+    if (p->halo_send_count[i] == 0) continue;
+    int j = -1;
+    for (int k = 0; k < b.n_peers; ++k)
+      if (b.peer_ids[k] == g->ids[0]) j = k;
+    if (j < 0 || b.recv_count[j] != p->halo_send_count[i])
+      return fail(RBF_ERR_PARAM, "halo lists of two parts disagree");
+    void *u0 = nullptr, *u1 = nullptr;
+    RBF_CK(cudaIpcOpenMemHandle(&u0, b.u0, cudaIpcMemLazyEnablePeerAccess));
+    g->ipc_opened.push_back(u0);
+    RBF_CK(cudaIpcOpenMemHandle(&u1, b.u1, cudaIpcMemLazyEnablePeerAccess));
+    g->ipc_opened.push_back(u1);
+    pa.peer[np].u[0] = static_cast<double*>(u0);
+    pa.peer[np].u[1] = static_cast<double*>(u1);
+    pa.peer[np].dst_off = b.recv_off[j];
+    pa.peer[np].src_off = p->halo_send_off[i];
+    pa.peer[np].count = p->halo_send_count[i];
+    ++np;
+  }
+  pa.n_peer = np;
+  pa.n_nbr = nn;
+  pa.sys_scope = 1;  // peers are other GPUs
+  if (g->fast_graph) {
+    cudaGraphExecDestroy(g->fast_graph);
+    g->fast_graph = nullptr;
+  }
+  g->push = true;
+  return RBF_OK;
+}
+
+int rbf_group_push_mode(const rbf_group* g) { return g && g->push ? 1 : 0; }
+
 void rbf_group_destroy(rbf_group* g) {
   if (!g) return;
   cudaSetDevice(g->device);
   if (g->stream) cudaStreamSynchronize(g->stream);
+  for (void* m : g->ipc_opened) cudaIpcCloseMemHandle(m);
+  for (unsigned int* t : g->tickets) cudaFree(t);
+  for (rbf_plan* p : g->parts) p->push = false;
   if (g->fast_graph) cudaGraphExecDestroy(g->fast_graph);
   if (g->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(g->comm);
   cudaFree(g->d_status);

@@ -233,6 +233,14 @@ struct rbf_plan {
   // partitioned runs (group.inc.cuh): exchange lists of this part
   std::vector<int> halo_peers;
   std::vector<int64_t> halo_send_count, halo_send_off, halo_recv_count, halo_recv_off;
+  // push-mode groups (group.inc.cuh): field buffers from cudaMalloc (IPC-exportable),
+  // this part's arrival counters (indexed by part id) and the neighbours to wait for
+  bool u_legacy = false;
+  bool push = false;
+  unsigned long long* push_flags = nullptr;
+  int wait_ids[rbf::kMaxPushPeers] = {};
+  int wait_n = 0;
+  int64_t push_base = 0;
   int* halo_send_idx = nullptr;     // [halo_send_total] local ids of owned nodes to send
   double* halo_sendbuf = nullptr;   // packed values, segments per peer
   int64_t halo_send_total = 0;
@@ -248,6 +256,9 @@ struct rbf_plan {
     a.st = st;
     a.C16 = C16;
     a.meta = meta;
+    a.wait_flags = push ? push_flags : nullptr;
+    a.wait_mask = 0;
+    for (int i = 0; push && i < wait_n; ++i) a.wait_mask |= 1ull << wait_ids[i];
     return a;
   }
 };
@@ -502,6 +513,8 @@ int reset_status(rbf_plan* p, double dt, double tol) {
   s.ticket = 0;
   s.dt = dt;
   s.tol = tol;
+  s.push_base = p->push_base;
+  s.push_count = 0;
   *p->h_st = s;
   RBF_CK(cudaMemcpyAsync(p->st, p->h_st, sizeof(s), cudaMemcpyHostToDevice, p->stream));
   return RBF_OK;
@@ -1892,8 +1905,15 @@ void rbf_plan_destroy(rbf_plan* p) {
   pool_free(p->W, s);
   pool_free(p->C, s);
   pool_free(p->F, s);
-  pool_free(p->U[0], s);
-  pool_free(p->U[1], s);
+  if (p->u_legacy) {
+    if (s) cudaStreamSynchronize(s);
+    cudaFree(p->U[0]);
+    cudaFree(p->U[1]);
+    cudaFree(p->push_flags);
+  } else {
+    pool_free(p->U[0], s);
+    pool_free(p->U[1], s);
+  }
   pool_free(p->tmp, s);
   pool_free(p->new_id, s);
   pool_free(p->row_of_k, s);

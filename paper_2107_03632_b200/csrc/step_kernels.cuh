@@ -125,7 +125,7 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
       const long long g0 = *reinterpret_cast<volatile long long*>(&st->step);
       const long long bs = *reinterpret_cast<volatile long long*>(&st->bad_step);
       const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
-      if ((bs >= 0 && bs < g0) || (cs >= 0 && cs < g0)) {
+      if (!a.wait_flags && ((bs >= 0 && bs < g0) || (cs >= 0 && cs < g0))) {
         for (long long i = 0; i < pre; ++i) mbar_wait(&full[i % stages], 0);  // drain the ring
         return;
       }
@@ -139,7 +139,7 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
       const long long g0 = *reinterpret_cast<volatile long long*>(&st->step);
       const long long bs = *reinterpret_cast<volatile long long*>(&st->bad_step);
       const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
-      if ((bs >= 0 && bs < g0) || (cs >= 0 && cs < g0)) return;
+      if (!a.wait_flags && ((bs >= 0 && bs < g0) || (cs >= 0 && cs < g0))) return;
     }
     gstep = *reinterpret_cast<volatile long long*>(&st->step);
   } else {
@@ -147,7 +147,8 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
     gstep = *reinterpret_cast<volatile long long*>(&st->step);
     const long long bs = *reinterpret_cast<volatile long long*>(&st->bad_step);
     const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
-    if ((bs >= 0 && bs < gstep) || (cs >= 0 && cs < gstep)) return;
+    if (!a.wait_flags && ((bs >= 0 && bs < gstep) || (cs >= 0 && cs < gstep))) return;
+    wait_peers(a.wait_flags, a.wait_mask, a.st, warp == 1, 32 * CW);
     const double dt = st->dt;
     const int units_per_chunk = sps / RPL;
     const long long total = my_n * units_per_chunk;  // consumer units of this CTA
@@ -776,6 +777,71 @@ __global__ void gather_field_kernel(const double* __restrict__ src, const int* _
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < N;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
     dst[i] = src[new_id[i]];
+}
+
+// ---------------------------------------------------------------------------
+// Push-mode halo exchange (group.inc.cuh): after a part's step, store the
+// owned values its neighbours read straight into their field buffers (P2P
+// stores over NVLink; plain device stores between the parts of one process),
+// then publish the arrival with one system-scope release store per neighbour.
+// Replaces pack + NCCL send/recv + their per-step launch latency.
+struct PushPeer {
+  double* u[2];        // the peer's field buffers (IPC-mapped or local)
+  long long dst_off;   // first slot of this part's halo group in the peer's numbering
+  long long src_off;   // first entry of the peer's segment in send_idx
+  long long count;
+};
+
+struct PushArgs {
+  const double* u[2];            // this part's field buffers
+  const int* send_idx;           // [total] owned local ids, segmented per peer
+  long long total;
+  int n_peer;                    // peers this part sends to
+  int n_nbr;                     // neighbours to notify (senders and receivers)
+  int my_id;
+  PushPeer peer[kMaxPushPeers];
+  unsigned long long* nbr_flags[kMaxPushPeers];  // neighbours' arrival arrays
+  DevStatus* st;
+  unsigned int* ticket;
+  int sys_scope;                 // 1: peers on other GPUs (fences at system scope)
+};
+
+__global__ void __launch_bounds__(256) push_halo_kernel(PushArgs a, int out) {
+  pdl_wait();  // the step that produced u[out] is complete and visible
+  pdl_launch_dependents();
+  const double* u = a.u[out];
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < a.total;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int i = 0;
+    while (i + 1 < a.n_peer && k >= a.peer[i + 1].src_off) ++i;
+    a.peer[i].u[out][a.peer[i].dst_off + (k - a.peer[i].src_off)] = u[a.send_idx[k]];
+  }
+  // the CTA's stores -> (barrier) -> one fence by thread 0 -> ticket; the last
+  // CTA's release store then publishes every CTA's stores (causality is
+  // transitive through the barrier, the fences and the ticket's RMW chain)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (a.sys_scope) __threadfence_system();
+    else __threadfence();
+    const unsigned int t = atomicAdd(a.ticket, 1u);
+    if (t == gridDim.x - 1) {
+      *a.ticket = 0u;
+      const long long v = a.st->push_base + (++a.st->push_count);
+      if (a.sys_scope) __threadfence_system();
+      else __threadfence();
+      for (int j = 0; j < a.n_nbr; ++j) {
+        if (a.sys_scope) {
+          asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.nbr_flags[j] + a.my_id),
+                       "l"(static_cast<unsigned long long>(v))
+                       : "memory");
+        } else {
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.nbr_flags[j] + a.my_id),
+                       "l"(static_cast<unsigned long long>(v))
+                       : "memory");
+        }
+      }
+    }
+  }
 }
 
 }  // namespace rbf

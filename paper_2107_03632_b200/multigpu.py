@@ -220,6 +220,26 @@ class _Group:
     def close(self):
         self._fin()
 
+    @property
+    def push_mode(self) -> bool:
+        """True when the fixed-step fast path pushes halos peer-to-peer."""
+        return bool(self._lib.rbf_group_push_mode(self._h))
+
+    def _push_local(self):
+        self.plans[0]._check(self._lib.rbf_group_push_local(self._h))
+
+    def _push_ipc(self, allgather):
+        """Exchange the push-mode blobs through `allgather(bytes) -> [bytes]`
+        (every rank's blob, e.g. torch.distributed.all_gather_object) and map
+        the neighbours' buffers.  The caller must barrier before running."""
+        buf = ctypes.create_string_buffer(1024)
+        n = ctypes.c_int64()
+        self.plans[0]._check(self._lib.rbf_group_push_export(self._h, buf, 1024, ctypes.byref(n)))
+        blobs = allgather(buf.raw[: n.value])
+        stride = max(len(b) for b in blobs)
+        flat = ctypes.create_string_buffer(b"".join(b.ljust(stride, b"\0") for b in blobs), stride * len(blobs))
+        self.plans[0]._check(self._lib.rbf_group_push_import(self._h, len(blobs), flat, stride))
+
     def run(self, dt, steps=0, mode="fixed", tol=1e-9, max_steps=1_000_000):
         from . import _lib
 
@@ -234,31 +254,36 @@ class _Group:
 
 
 class LocalGroup(_Group):
-    """All parts in this process (one GPU or several): halos move by device copy.
+    """All parts in this process (one GPU): the single-process form of the
+    partitioned loop.  Fixed-step runs push halos straight into the peers'
+    buffers after each part's step (push mode, the default); steady runs and
+    failure replays use pack / device copy / step / reduce on one stream."""
 
-    This is the single-process form of the partitioned loop: the same pack /
-    exchange / step / reduce sequence as the NCCL group, with
-    cudaMemcpyPeerAsync in place of send/recv, run in order on one stream.
-    """
-
-    def __init__(self, parts: Sequence[Part], devices: Optional[Sequence[int]] = None):
+    def __init__(self, parts: Sequence[Part], devices: Optional[Sequence[int]] = None, push: bool = True):
         from .solver import Plan
 
         devices = list(devices) if devices is not None else [0] * len(parts)
         plans = [Plan(pt.n_local, pt.interior, pt.rows, pt.weights, pt.f_int, device=d,
                       resident=False) for pt, d in zip(parts, devices)]
         super().__init__(parts, plans, None, 0, 1)
+        if push and len(parts) > 1:
+            self._push_local()
 
 
 class NcclGroup(_Group):
-    """One part per process / GPU; halos over NCCL (NVLink), launched with torchrun."""
+    """One part per process / GPU, launched with torchrun.  With `allgather`
+    (bytes -> every rank's bytes) the fixed-step fast path pushes halos over
+    NVLink through CUDA IPC mappings of the peers' buffers; steady runs and
+    failure replays exchange by NCCL send/recv."""
 
-    def __init__(self, part: Part, rank: int, nranks: int, device: int, uid: bytes):
+    def __init__(self, part: Part, rank: int, nranks: int, device: int, uid: bytes, allgather=None):
         from .solver import Plan
 
         plan = Plan(part.n_local, part.interior, part.rows, part.weights, part.f_int,
                     device=device, resident=False)
         super().__init__([part], [plan], uid, rank, nranks)
+        if allgather is not None and nranks > 1:
+            self._push_ipc(allgather)
 
 
 def nccl_unique_id() -> bytes:

@@ -636,6 +636,42 @@ def test_partitioned_group_instability_and_synthetic(golden, synth_cache):
     group.close()
 
 
+@pytest.mark.parametrize("push", [True, False], ids=["p2p-push", "copy-exchange"])
+@pytest.mark.parametrize("P", [2, 5])
+def test_partitioned_push_mode_runs(synth_cache, push, P):
+    """Push-mode halos (push_halo_kernel stores into the peers' buffers and
+    signals arrivals; the next step waits on them) against the copy exchange
+    and the oracle, over repeated runs (the arrival counters keep counting
+    across runs), odd step counts and graph-chunked runs."""
+    from paper_2107_03632_b200.multigpu import LocalGroup, partition, run_partitioned
+
+    nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
+    interior = shapes.interior_nodes
+    parts = partition(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                      rb.forcing(nodes.positions[interior]), nodes.positions, P)
+    group = LocalGroup(parts, push=push)
+    assert group.push_mode == push
+    for steps in (50, 37, 131, 2):
+        cfg = rb.SolveConfig(degree=2, support_size=15, nodes=200_000, steps=steps)
+        field, done, residual, _, _ = run_partitioned(group, nodes, shapes, cfg)
+        want = orc.run_time_loop(nodes, shapes, steps=steps)
+        assert done == steps and residual == want["residual"], steps
+        assert np.array_equal(field, want["field"]), steps
+    # a failure inside a pushed run replays on the exact path (same step as the oracle)
+    cfg = rb.SolveConfig(degree=2, support_size=15, nodes=200_000, steps=300, dt=40.0 * rb.stability_bound(shapes))
+    want = orc.run_time_loop(nodes, shapes, dt=cfg.dt, steps=300)
+    with pytest.raises(rb.InstabilityError) as ei:
+        run_partitioned(group, nodes, shapes, cfg)
+    assert ei.value.step == want["step"]
+    # and the group keeps working (pushing) afterwards
+    cfg = rb.SolveConfig(degree=2, support_size=15, nodes=200_000, steps=65)
+    field, _, residual, _, _ = run_partitioned(group, nodes, shapes, cfg)
+    want = orc.run_time_loop(nodes, shapes, steps=65)
+    assert np.array_equal(field, want["field"]) and residual == want["residual"]
+    assert group.push_mode == push
+    group.close()
+
+
 @pytest.mark.parametrize("n_rows", [1, 33, 100])
 def test_streaming_variants_on_tiny_row_counts(n_rows):
     """Partial last slices and single-row problems through every loop variant."""

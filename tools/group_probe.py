@@ -1,0 +1,45 @@
+"""Partitioned loop on one GPU: per-step cost of the halo exchange modes.
+
+All parts run in order on one device, so a P-part step costs the sum of the
+parts' steps plus the exchange: compare against one plan over all rows.
+"""
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import paper_2107_03632_b200 as rb  # noqa: E402
+from paper_2107_03632_b200 import synth  # noqa: E402
+from paper_2107_03632_b200.multigpu import LocalGroup, partition  # noqa: E402
+
+target = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1_000_000
+nodes, st, sh = synth.synthetic_problem(target, 15, 2, weights="gpu")
+interior = sh.interior_nodes
+rows = st.neighbors[interior]
+f = rb.forcing(nodes.positions[interior])
+u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+dt = 0.5 * rb.stability_bound(sh)
+steps = 2000
+plan = rb.Plan(nodes.n_total, interior, rows, sh.weights, f, nodes.positions, renumber=True, pair=False)
+plan.set_field(u0)
+plan.run(dt, steps=100)
+t1 = min(plan.run(dt, steps=steps).device_seconds for _ in range(3)) / steps
+print(f"N={nodes.n_total} one plan: {1e6 * t1:.2f} us/step", flush=True)
+for P in (2, 4):
+    parts = partition(nodes.n_total, interior, rows, sh.weights, f, nodes.positions, P)
+    for push in (True, False):
+        g = LocalGroup(parts, push=push)
+        for part, p in zip(parts, g.plans):
+            p.set_field(part.local_field(u0))
+        g.run(dt, steps=100)
+        best = 1e9
+        for _ in range(3):
+            for part, p in zip(parts, g.plans):
+                p.set_field(part.local_field(u0))
+            rc, done, res, bad, sec = g.run(dt, steps=steps)
+            best = min(best, sec / steps)
+        halo = sum(pt.halo_bytes_per_step() for pt in parts)
+        print(f"  P={P} {'push' if push else 'copy'}: {1e6 * best:.2f} us/step for all parts "
+              f"(+{1e6 * (best - t1):.2f} us vs one plan; halo {halo / 1e3:.0f} kB/step)", flush=True)
+        g.close()
