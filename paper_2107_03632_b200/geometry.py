@@ -13,6 +13,7 @@ geometry.py:74-102).
 
 from __future__ import annotations
 
+import csv
 import ctypes
 import operator
 
@@ -33,11 +34,17 @@ __all__ = [
     "NodeSet",
     "closed_form_solution",
     "forcing",
+    "BOUNDARY_TOL",
     "generate_unit_disk_nodes",
+    "load_nodes_csv",
     "node_count_for_spacing",
+    "save_nodes_csv",
     "seed_key",
     "spacing_for_node_count",
 ]
+
+
+BOUNDARY_TOL = 1e-12  # geometry.py:23: | ||p|| - 1 | tolerance of boundary nodes
 
 
 def seed_key(seed: int) -> np.ndarray:
@@ -82,3 +89,24 @@ def generate_unit_disk_nodes(h: float, seed: int = 0) -> NodeSet:
     is_boundary = np.zeros(N, dtype=bool)
     is_boundary[: n_boundary.value] = True
     return NodeSet(positions=positions, is_boundary=is_boundary, h=h)
+
+
+def save_nodes_csv(nodes: NodeSet, path) -> None:
+    """CSV with header x,y,kind, %.17g coordinates (geometry.py:200-206)."""
+    with open(path, "w", newline="") as fh:
+        writer = csv.writer(fh)
+        writer.writerow(["x", "y", "kind"])
+        for (x, y), b in zip(nodes.positions, nodes.is_boundary):
+            writer.writerow([f"{x:.17g}", f"{y:.17g}", "boundary" if b else "interior"])
+
+
+def load_nodes_csv(path, h: float = float("nan")) -> NodeSet:
+    """Read a node set written by save_nodes_csv (geometry.py:209-219)."""
+    xs, ys, kinds = [], [], []
+    with open(path, newline="") as fh:
+        for row in csv.DictReader(fh):
+            xs.append(float(row["x"]))
+            ys.append(float(row["y"]))
+            kinds.append(row["kind"] == "boundary")
+    positions = np.column_stack([np.asarray(xs, dtype=float), np.asarray(ys, dtype=float)])
+    return NodeSet(positions=positions.reshape(-1, 2), is_boundary=np.asarray(kinds, dtype=bool), h=h)

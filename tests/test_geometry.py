@@ -80,3 +80,47 @@ def test_determinism_and_spacing():
     assert d[:, 1].min() >= 0.8 * h * (1 - 1e-12)
     assert abs(a.n_total - rb.node_count_for_spacing(h)) < 0.1 * a.n_total
     assert math.isclose(a.h, h)
+
+
+# ---- the reference's own geometry tests (pkg/tests/test_geometry.py:53-129) ----
+def test_node_count_for_spacing_values():
+    assert rb.node_count_for_spacing(0.055) == 1153
+    assert rb.node_count_for_spacing(0.1) == 377
+    assert rb.node_count_for_spacing(0.01) / rb.node_count_for_spacing(0.02) == pytest.approx(4.0, rel=0.05)
+
+
+@pytest.mark.parametrize("h", [0.6, 0.5, 0.0, -0.1])
+def test_node_count_rejects_bad_spacing(h):
+    with pytest.raises(rb.ParameterError):
+        rb.node_count_for_spacing(h)
+
+
+def test_spacing_for_node_count_inverts_estimate():
+    for target in (100, 500, 1027, 10_000):
+        assert rb.node_count_for_spacing(rb.spacing_for_node_count(target)) == pytest.approx(target, abs=1)
+
+
+def test_generate_counts_classification_and_separation():
+    h = 0.1
+    nodes = geometry.generate_unit_disk_nodes(h, seed=1)
+    assert nodes.n_total == nodes.n_interior + nodes.n_boundary and nodes.n_interior >= 1
+    assert nodes.n_boundary == round(2 * math.pi / h)
+    radii = np.linalg.norm(nodes.positions, axis=1)
+    assert np.all(np.abs(radii[nodes.is_boundary] - 1.0) <= geometry.BOUNDARY_TOL)
+    assert np.all(radii[~nodes.is_boundary] < 1.0 - geometry.BOUNDARY_TOL)
+    c = geometry.generate_unit_disk_nodes(h, seed=8)
+    assert not np.array_equal(nodes.positions[:50], c.positions[:50]) or nodes.n_total != c.n_total
+    pts = geometry.generate_unit_disk_nodes(0.12, seed=2).positions
+    dist = np.sqrt(((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1))
+    dist[np.diag_indices_from(dist)] = np.inf
+    assert dist.min() >= 0.5 * 0.12
+
+
+def test_nodes_csv_roundtrip(tmp_path):
+    nodes = geometry.generate_unit_disk_nodes(0.15, seed=4)
+    path = tmp_path / "nodes.csv"
+    geometry.save_nodes_csv(nodes, path)
+    assert path.read_text().splitlines()[0] == "x,y,kind"
+    loaded = geometry.load_nodes_csv(path)
+    assert np.array_equal(loaded.positions, nodes.positions)
+    assert np.array_equal(loaded.is_boundary, nodes.is_boundary)
