@@ -356,7 +356,9 @@ def main():
             "loop": {0: "resident on-chip loop (one CTA)",
                      1: "streaming step (plain loads), CUDA graphs of 64 steps",
                      2: "streaming step (TMA bulk-copy ring, warp-specialised), CUDA graphs of 64 steps",
-                     3: "cluster-resident loop (thread-block cluster, DSMEM halo, one launch)"}[
+                     3: "cluster-resident loop (thread-block cluster, DSMEM halo, one launch)",
+                     4: "grid-resident loop (rows in every SM's shared memory, one cooperative launch, "
+                        "grid barrier per step)"}[
                          info["variant"]] + ("" if args.no_pdl or info["resident"] else " + PDL"),
             "parallelism": "single GPU",
         },

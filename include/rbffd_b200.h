@@ -202,8 +202,10 @@ typedef struct rbf_plan_info {
   int32_t kernel_n;        /* compile-time width of the chosen step kernel (0: generic) */
   int32_t grid, block;     /* streaming kernel launch geometry */
   int32_t variant;         /* 0 resident loop (1 CTA), 1 LDG streaming step, 2 TMA-ring
-                              streaming step, 3 cluster-resident loop (DSMEM halo); fixed-step
-                              runs of variant 2 use the persistent dataflow loop when flow == 1 */
+                              streaming step, 3 cluster-resident loop (DSMEM halo), 4 grid-resident
+                              loop (rows in every SM's shared memory, one cooperative launch);
+                              fixed-step runs of variant 2 use the persistent dataflow loop when
+                              flow == 1 */
   int32_t index_bits;      /* 32, or 16: two-window 16-bit ids streamed by the TMA step */
   int32_t flow;            /* 1: fixed-step runs use the persistent dataflow loop */
   int32_t flow_grid;       /* its CTAs (one per SM) */

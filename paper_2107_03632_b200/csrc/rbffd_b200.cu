@@ -79,6 +79,7 @@ using TmaFn = void (*)(rbf::StepArgs, const double*, double*, int, rbf::TmaGeom)
 using ResidentFn = void (*)(rbf::ResidentArgs);
 using ClusterFn = void (*)(rbf::ClusterArgs);
 using FlowFn = void (*)(rbf::FlowArgs, rbf::TmaGeom);
+using GridFn = void (*)(rbf::GridArgs);
 
 template <int NJ>
 struct KernelSet {
@@ -114,6 +115,10 @@ struct KernelSet {
     }
   }
   static int cw() { return kCW; }
+  static GridFn grid() {
+    if constexpr (NJ > 0) return rbf::grid_loop_kernel<NJ>;
+    else return nullptr;
+  }
 };
 
 // Support sizes with a fully unrolled instantiation; others use the generic
@@ -201,6 +206,10 @@ struct rbf_plan {
   int tma_block = 0;
   int variant = 1;                 // 0 resident, 1 LDG streaming, 2 TMA streaming, 3 cluster loop
   ClusterFn cluster_fn = nullptr;  // non-null: the loop runs in one thread-block cluster
+  GridFn grid_fn = nullptr;        // non-null: the loop runs in one cooperative grid (rows in smem)
+  int grid_ctas = 0, grid_spc = 0;
+  size_t grid_smem = 0;
+  unsigned long long* grid_red = nullptr;  // [3][2] per-step partial slots
   int cluster_q = 0, cluster_rpc = 0, cluster_threads = 0;
   size_t cluster_smem = 0;
   unsigned int* cluster_dest = nullptr;
@@ -746,6 +755,33 @@ int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
                    p->cluster_q, double(h[0]) / limit, double(h[1]) / limit, double(h[2]) / limit,
                    double(h[3]) / limit);
     }
+  } else if (limit > 0 && p->N_i > 0 && p->grid_fn) {
+    rbf::GridArgs a;
+    a.W = p->W;
+    a.C = p->C;
+    a.F = p->F;
+    a.U0 = p->U[0];
+    a.U1 = p->U[1];
+    a.n_rows = p->N_i;
+    a.dst_base = p->B;
+    a.limit = limit;
+    a.spc = p->grid_spc;
+    a.flags = steady ? rbf::kSteady : 0;
+    a.st = p->st;
+    a.red = p->grid_red;
+    RBF_CK(cudaMemsetAsync(p->grid_red, 0, 7 * sizeof(unsigned long long), p->stream));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p->grid_ctas);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = p->grid_smem;
+    cfg.stream = p->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: grid barrier per step
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RBF_CK(cudaLaunchKernelEx(&cfg, p->grid_fn, a));
+    ++p->launches;
   } else if (limit > 0 && p->N_i > 0) {
     rbf::ResidentArgs a;
     a.W = p->W;
@@ -951,7 +987,38 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
   }
   int sms = 148, per_sm = 1;
   RBF_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  p->variant = p->cluster_fn ? 3 : (p->resident ? 0 : 1);
+  // grid-resident loop: every SM holds its share of the rows in shared memory
+  const char* grid_env = std::getenv("RBFFD_GRID");
+  if (!p->resident && !(flags & RBF_NO_RESIDENT) && N_i > 0 && !(grid_env && std::atoi(grid_env) == 0)) {
+    GridFn gfn = nullptr;
+    switch (n) {
+#define RBF_GCASE(K) \
+  case K:            \
+    gfn = KernelSet<K>::grid(); \
+    break;
+      RBF_SPECIALISED(RBF_GCASE)
+#undef RBF_GCASE
+      default:
+        break;
+    }
+    const int64_t spc = (p->S + sms - 1) / sms;
+    const size_t gsmem = static_cast<size_t>(spc) * (static_cast<size_t>(n) * 32 * 12 + 32 * 8);
+    int optin = 0;
+    RBF_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    if (gfn && gsmem + 1024 <= static_cast<size_t>(optin) && set_max_smem(gfn) == cudaSuccess) {
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gfn, 512, gsmem) == cudaSuccess && occ >= 1) {
+        RBF_TRY(dev_alloc(p.get(), &p->grid_red, 7));
+        p->grid_fn = gfn;
+        p->grid_spc = static_cast<int>(spc);
+        p->grid_ctas = static_cast<int>((p->S + spc - 1) / spc);
+        p->grid_smem = gsmem;
+        p->resident = true;
+      }
+    }
+    cudaGetLastError();
+  }
+  p->variant = p->grid_fn ? 4 : (p->cluster_fn ? 3 : (p->resident ? 0 : 1));
   if (tma_fn && !(flags & RBF_STREAM_LDG) && N_i > 0) {
     // ring geometry: ~24 KB stages, as many as fit in ~200 KB of shared memory
     const int slice = n * 32 * (8 + p->index_bits / 8) + 32 * 8 + (p->index_bits == 16 ? 16 : 0);
@@ -1919,6 +1986,7 @@ void rbf_plan_destroy(rbf_plan* p) {
   pool_free(p->row_of_k, s);
   pool_free(p->halo_send_idx, s);
   pool_free(p->cluster_dest, s);
+  pool_free(p->grid_red, s);
   pool_free(p->C16, s);
   pool_free(p->meta, s);
   pool_free(p->flow_flags, s);

@@ -602,6 +602,158 @@ __global__ void __launch_bounds__(MAXT, 1) cluster_loop_kernel(ClusterArgs a) {
   cluster.sync();  // no CTA leaves while a peer may still address its shared memory
 }
 
+// ---------------------------------------------------------------------------
+// Grid-resident loop for mid-size problems (too big for one cluster's shared
+// memory, small enough that every SM can hold its share of the rows): one
+// cooperative launch runs every step.  Each CTA copies its contiguous range
+// of SELL slices (weights, ids, forcing) into shared memory once; the field
+// stays in global memory (L2-resident at these sizes, double-buffered); one
+// grid barrier per step publishes the new values and the per-step
+// non-finite / residual partials (three rotating slots, so a slot is reset
+// two barriers after it was read).  Removes the per-step launch, ring fill
+// and weight stream of the streaming path.  Arithmetic and j-order are those
+// of row_update (bitwise parity).
+struct GridArgs {
+  const double* W;
+  const int* C;
+  const double* F;
+  double* U0;  // start field in U0; the final field is published into both
+  double* U1;
+  long long n_rows, dst_base, limit;
+  int spc;     // slices per CTA
+  int flags;   // kSteady
+  DevStatus* st;
+  unsigned long long* red;  // [0..2] residual bits max per step slot, [6] the grid
+                            // barrier's arrival counter (+2^40 per non-finite CTA-step)
+};
+
+template <int NJ>
+__global__ void __launch_bounds__(512, 1) grid_loop_kernel(GridArgs a) {
+  extern __shared__ __align__(16) unsigned char gl_smem[];
+  const long long S = (a.n_rows + 31) >> 5;
+  const long long s0 = static_cast<long long>(blockIdx.x) * a.spc;
+  const long long s1 = s0 + a.spc < S ? s0 + a.spc : S;
+  const int ns = s1 > s0 ? static_cast<int>(s1 - s0) : 0;
+  double* sW = reinterpret_cast<double*>(gl_smem);
+  double* sF = sW + static_cast<size_t>(a.spc) * NJ * 32;
+  int* sC = reinterpret_cast<int*>(sF + static_cast<size_t>(a.spc) * 32);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  {
+    const long long e0 = s0 * NJ * 32, ne = static_cast<long long>(ns) * NJ * 32;
+    for (long long e = tid; e < ne; e += blockDim.x) {
+      sW[e] = a.W[e0 + e];
+      sC[e] = a.C[e0 + e];
+    }
+    for (long long e = tid; e < static_cast<long long>(ns) * 32; e += blockDim.x) sF[e] = a.F[s0 * 32 + e];
+  }
+  __shared__ unsigned long long s_max[16];
+  __shared__ unsigned int s_bad[16];
+  DevStatus* st = a.st;
+  const double dt = st->dt, tol = st->tol;
+  const bool steady = (a.flags & kSteady) != 0;
+  long long step = 0, bad_step = -1, conv_step = -1, last_res_step = -1;
+  unsigned long long last_bits = 0;
+  int cur = 0;
+  __syncthreads();
+  for (; step < a.limit; ++step) {
+    const bool need_res = steady || step == a.limit - 1;
+    const double* uc = cur ? a.U1 : a.U0;
+    double* un = cur ? a.U0 : a.U1;
+    bool bad = false;
+    unsigned long long dmax = 0ull;
+    for (int k = warp; k < ns; k += nwarps) {
+      const long long r = (s0 + k) * 32 + lane;
+      if (r >= a.n_rows) continue;
+      const double* w = sW + static_cast<size_t>(k) * NJ * 32 + lane;
+      const int* c = sC + static_cast<size_t>(k) * NJ * 32 + lane;
+      double g[NJ];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) g[j] = uc[c[32 * j]];
+      const long long node = a.dst_base + r;
+      const double u_self = (c[0] == node) ? g[0] : uc[node];
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(w[32 * j], g[j]));
+      const double value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(sF[k * 32 + lane], acc)));
+      un[node] = value;
+      bad |= !isfinite(value);
+      if (need_res) {
+        const unsigned long long b =
+            static_cast<unsigned long long>(__double_as_longlong(fabs(__dsub_rn(value, u_self))));
+        dmax = b > dmax ? b : dmax;
+      }
+    }
+    // CTA partials.  The non-finite flag rides on the barrier arrival (the
+    // counter's high bits count non-finite CTA-steps; the loop stops at the
+    // first, so any high bit means "this step"); the residual max goes to
+    // this step's slot, the slot two steps ahead is reset by CTA 0.
+    const unsigned int wb = __reduce_or_sync(0xffffffffu, bad ? 1u : 0u);
+    const unsigned long long wm = need_res ? warp_max_u64(dmax) : 0ull;
+    if (lane == 0) {
+      s_bad[warp] = wb;
+      s_max[warp] = wm;
+    }
+    __syncthreads();
+    const int slot = static_cast<int>(step % 3);
+    constexpr unsigned long long kArrive = 1ull, kBad = 1ull << 40;
+    __shared__ unsigned long long s_seen;
+    if (tid == 0) {
+      unsigned int cb = 0;
+      unsigned long long cm = 0ull;
+      for (int w = 0; w < nwarps; ++w) {
+        cb |= s_bad[w];
+        cm = s_max[w] > cm ? s_max[w] : cm;
+      }
+      if (need_res && cm) atomicMax(&a.red[slot], cm);
+      if (blockIdx.x == 0) a.red[(step + 1) % 3] = 0ull;
+      // grid barrier on a monotonic arrival counter: the fence publishes the
+      // CTA's field stores (ordered after the CTA barrier above), the acquire
+      // spin orders every CTA's reads of the new field after all arrivals
+      __threadfence();
+      atomicAdd(&a.red[6], kArrive + (cb ? kBad : 0ull));
+      const unsigned long long target = static_cast<unsigned long long>(step + 1) * gridDim.x;
+      unsigned long long v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&a.red[6]) : "memory");
+      } while ((v & (kBad - 1)) < target);
+      s_seen = v;
+    }
+    __syncthreads();
+    const bool gbad = (s_seen >> 40) != 0;
+    const unsigned long long gmax =
+        need_res ? *reinterpret_cast<volatile unsigned long long*>(&a.red[slot]) : 0ull;
+    cur ^= 1;
+    if (gbad) {
+      bad_step = step;
+      break;
+    }
+    if (need_res) {
+      last_bits = gmax;
+      last_res_step = step;
+      if (steady && __ddiv_rn(__longlong_as_double(static_cast<long long>(gmax)), dt) <= tol) {
+        conv_step = step;
+        ++step;
+        break;
+      }
+    }
+  }
+  // the field after the last executed step (after a failure: its u2) is in
+  // buffer `cur`; publish it into both buffers
+  const double* uf = cur ? a.U1 : a.U0;
+  double* uo = cur ? a.U0 : a.U1;
+  for (int k = warp; k < ns; k += nwarps) {
+    const long long r = (s0 + k) * 32 + lane;
+    if (r < a.n_rows) uo[a.dst_base + r] = uf[a.dst_base + r];
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    st->bad_step = bad_step;
+    st->conv_step = conv_step;
+    st->last_res_bits = last_bits;
+    st->last_res_step = last_res_step;
+    st->step = (bad_step >= 0) ? bad_step + 1 : step;
+  }
+}
+
 // dest[row(c)] |= 1 << owner(r) for every stencil entry c of row r that is an
 // interior node owned by another CTA of the cluster (owner(r) = r / rpc)
 __global__ void cluster_dest_kernel(const int* __restrict__ C, long long n_rows, int n, long long B,

@@ -330,7 +330,7 @@ def test_tma_and_ldg_step_variants_agree_with_oracle(synth_cache, target, n, m):
                                   (True, True, True, False), (True, False, True, False),
                                   (True, True, False, False), (False, True, True, True)):
         plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, nodes.positions,
-                    renumber=True, tma=tma, pdl=pdl, idx16=idx16, flow=flow)
+                    renumber=True, tma=tma, pdl=pdl, idx16=idx16, flow=flow, resident=False)
         info = plan.info()
         assert info["variant"] == (2 if tma else 1)
         assert info["index_bits"] == (16 if (tma and idx16 and n <= 32) else 32)
@@ -455,6 +455,47 @@ def test_every_width_matches_oracle(n):
         plan.close()
 
 
+# ---- grid-resident loop (rows in every SM's shared memory) -------------------
+@pytest.mark.parametrize("target,n,m", [(20_000, 15, 2), (150_000, 15, 2), (60_000, 30, 4), (20_000, 56, 6)])
+def test_grid_loop_matches_oracle(synth_cache, target, n, m):
+    """One cooperative launch for all steps: fixed runs of every length, swap
+    and copy-back, continued runs, steady mode, and the failure step."""
+    nodes, _, shapes = _synth(synth_cache, target, n, m)
+    interior = shapes.interior_nodes
+    plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                rb.forcing(nodes.positions[interior]), nodes.positions, renumber=True)
+    assert plan.info()["variant"] == 4 and plan.info()["resident"] == 1
+    u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    dt = 0.5 * rb.stability_bound(shapes)
+    for steps in (1, 2, 3, 130):
+        want = orc.run_time_loop(nodes, shapes, steps=steps)
+        for copy_back in (False, True):
+            plan.set_field(u0)
+            res = plan.run(dt, steps=steps, copy_back=copy_back)
+            assert res.steps_done == steps and res.residual == want["residual"], (steps, copy_back)
+            assert np.array_equal(plan.get_field(), want["field"]), (steps, copy_back)
+    plan.set_field(u0)
+    plan.run(dt, steps=20)
+    plan.run(dt, steps=21)
+    want = orc.run_time_loop(nodes, shapes, steps=41)
+    assert np.array_equal(plan.get_field(), want["field"])
+    # steady: stop step, residual and field are the oracle's
+    want = orc.run_time_loop(nodes, shapes, mode="steady", tol=5e-2, max_steps=20_000)
+    plan.set_field(u0)
+    res = plan.run(dt, mode="steady", tol=5e-2, max_steps=20_000)
+    assert res.steps_done == want["steps"] and res.residual == want["residual"]
+    assert np.array_equal(plan.get_field(), want["field"])
+    # instability: the reference's failing step and its field
+    dtb = 40.0 * dt
+    want = orc.run_time_loop(nodes, shapes, dt=dtb, steps=400)
+    assert want["status"] == orc.ORC_INSTABILITY
+    plan.set_field(u0)
+    res = plan.run(dtb, steps=400)
+    assert res.status == _lib.RBF_ERR_INSTABILITY and res.bad_step == want["step"]
+    assert np.array_equal(plan.get_field(), want["field"], equal_nan=True)
+    plan.close()
+
+
 # ---- two steps per launch (pair_kernels.cu) ---------------------------------
 @pytest.mark.parametrize("target,n,m", [(20_000, 15, 2), (20_000, 30, 4), (200_000, 15, 2), (50_000, 12, 2)])
 @pytest.mark.parametrize("renumber", [False, True], ids=["native", "morton"])
@@ -464,7 +505,8 @@ def test_pair_kernel_matches_oracle(synth_cache, target, n, m, renumber):
     nodes, _, shapes = _synth(synth_cache, target, n, m)
     interior = shapes.interior_nodes
     plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
-                rb.forcing(nodes.positions[interior]), nodes.positions, renumber=renumber, pair=True)
+                rb.forcing(nodes.positions[interior]), nodes.positions, renumber=renumber, pair=True,
+                resident=False)
     info = plan.info()
     assert info["pair"] == 1 and info["pair_tiles"] > 0 and info["pair_halo_rows"] > 0
     u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
@@ -505,7 +547,8 @@ def test_pair_kernel_failure_replays_the_exact_step(synth_cache):
     nodes, _, shapes = _synth(synth_cache, 20_000, 15, 2)
     interior = shapes.interior_nodes
     plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
-                rb.forcing(nodes.positions[interior]), nodes.positions, renumber=True, pair=True)
+                rb.forcing(nodes.positions[interior]), nodes.positions, renumber=True, pair=True,
+                resident=False)
     dt = 40.0 * rb.stability_bound(shapes)
     want = orc.run_time_loop(nodes, shapes, dt=dt, steps=400)
     assert want["status"] == orc.ORC_INSTABILITY
