@@ -207,7 +207,7 @@ struct rbf_plan {
   int variant = 1;                 // 0 resident, 1 LDG streaming, 2 TMA streaming, 3 cluster loop
   ClusterFn cluster_fn = nullptr;  // non-null: the loop runs in one thread-block cluster
   GridFn grid_fn = nullptr;        // non-null: the loop runs in one cooperative grid (rows in smem)
-  int grid_ctas = 0, grid_spc = 0;
+  int grid_ctas = 0, grid_spc = 0, grid_spr = 0;
   size_t grid_smem = 0;
   unsigned long long* grid_red = nullptr;  // [3][2] per-step partial slots
   int cluster_q = 0, cluster_rpc = 0, cluster_threads = 0;
@@ -766,6 +766,7 @@ int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
     a.dst_base = p->B;
     a.limit = limit;
     a.spc = p->grid_spc;
+    a.spr = p->grid_spr;
     a.flags = steady ? rbf::kSteady : 0;
     a.st = p->st;
     a.red = p->grid_red;
@@ -1001,16 +1002,24 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
       default:
         break;
     }
+    // rows beyond what shared memory holds are re-read every step from L2
+    // (evict_last); allowed while that part stays well inside the L2
     const int64_t spc = (p->S + sms - 1) / sms;
-    const size_t gsmem = static_cast<size_t>(spc) * (static_cast<size_t>(n) * 32 * 12 + 32 * 8);
+    const size_t slice_bytes = static_cast<size_t>(n) * 32 * 12 + 32 * 8;
     int optin = 0;
     RBF_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-    if (gfn && gsmem + 1024 <= static_cast<size_t>(optin) && set_max_smem(gfn) == cudaSuccess) {
+    const int64_t spr = std::min<int64_t>(spc, static_cast<int64_t>((static_cast<size_t>(optin) - 2048) / slice_bytes));
+    const size_t gsmem = static_cast<size_t>(spr) * slice_bytes;
+    const double l2_part = static_cast<double>(std::max<int64_t>(0, p->S - spr * sms)) * slice_bytes;
+    double l2_cap = 88.0e6;  // measured crossover ~90-100 MB (profiles/README.md)
+    if (const char* e = std::getenv("RBFFD_GRID_L2_MB")) l2_cap = std::atof(e) * 1.0e6;
+    if (gfn && spr >= 1 && l2_part <= l2_cap && set_max_smem(gfn) == cudaSuccess) {
       int occ = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gfn, 512, gsmem) == cudaSuccess && occ >= 1) {
         RBF_TRY(dev_alloc(p.get(), &p->grid_red, 7));
         p->grid_fn = gfn;
         p->grid_spc = static_cast<int>(spc);
+        p->grid_spr = static_cast<int>(spr);
         p->grid_ctas = static_cast<int>((p->S + spc - 1) / spc);
         p->grid_smem = gsmem;
         p->resident = true;

@@ -621,6 +621,8 @@ struct GridArgs {
   double* U1;
   long long n_rows, dst_base, limit;
   int spc;     // slices per CTA
+  int spr;     // of which held in shared memory; the rest is re-read every step
+               // from global memory, kept L2-resident (evict_last)
   int flags;   // kSteady
   DevStatus* st;
   unsigned long long* red;  // [0..2] residual bits max per step slot, [6] the grid
@@ -635,16 +637,18 @@ __global__ void __launch_bounds__(512, 1) grid_loop_kernel(GridArgs a) {
   const long long s1 = s0 + a.spc < S ? s0 + a.spc : S;
   const int ns = s1 > s0 ? static_cast<int>(s1 - s0) : 0;
   double* sW = reinterpret_cast<double*>(gl_smem);
-  double* sF = sW + static_cast<size_t>(a.spc) * NJ * 32;
-  int* sC = reinterpret_cast<int*>(sF + static_cast<size_t>(a.spc) * 32);
+  double* sF = sW + static_cast<size_t>(a.spr) * NJ * 32;
+  int* sC = reinterpret_cast<int*>(sF + static_cast<size_t>(a.spr) * 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int nres = ns < a.spr ? ns : a.spr;  // slices held in shared memory
+  const uint64_t pol_keep = policy_evict_last();
   {
-    const long long e0 = s0 * NJ * 32, ne = static_cast<long long>(ns) * NJ * 32;
+    const long long e0 = s0 * NJ * 32, ne = static_cast<long long>(nres) * NJ * 32;
     for (long long e = tid; e < ne; e += blockDim.x) {
       sW[e] = a.W[e0 + e];
       sC[e] = a.C[e0 + e];
     }
-    for (long long e = tid; e < static_cast<long long>(ns) * 32; e += blockDim.x) sF[e] = a.F[s0 * 32 + e];
+    for (long long e = tid; e < static_cast<long long>(nres) * 32; e += blockDim.x) sF[e] = a.F[s0 * 32 + e];
   }
   __shared__ unsigned long long s_max[16];
   __shared__ unsigned int s_bad[16];
@@ -664,17 +668,35 @@ __global__ void __launch_bounds__(512, 1) grid_loop_kernel(GridArgs a) {
     for (int k = warp; k < ns; k += nwarps) {
       const long long r = (s0 + k) * 32 + lane;
       if (r >= a.n_rows) continue;
-      const double* w = sW + static_cast<size_t>(k) * NJ * 32 + lane;
-      const int* c = sC + static_cast<size_t>(k) * NJ * 32 + lane;
-      double g[NJ];
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) g[j] = uc[c[32 * j]];
       const long long node = a.dst_base + r;
-      const double u_self = (c[0] == node) ? g[0] : uc[node];
-      double acc = 0.0;
+      double acc = 0.0, u_self, fk;
+      if (k < nres) {  // rows held in shared memory
+        const double* w = sW + static_cast<size_t>(k) * NJ * 32 + lane;
+        const int* c = sC + static_cast<size_t>(k) * NJ * 32 + lane;
+        double g[NJ];
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(w[32 * j], g[j]));
-      const double value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(sF[k * 32 + lane], acc)));
+        for (int j = 0; j < NJ; ++j) g[j] = uc[c[32 * j]];
+        u_self = (c[0] == node) ? g[0] : uc[node];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(w[32 * j], g[j]));
+        fk = sF[k * 32 + lane];
+      } else {  // rows re-read from L2 every step
+        const long long e = (s0 + k) * NJ * 32 + lane;
+        int c[NJ];
+        double w[NJ], g[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          c[j] = ld_stream_s32(a.C + e + 32 * j, pol_keep);
+          w[j] = ld_stream_f64(a.W + e + 32 * j, pol_keep);
+        }
+        fk = ld_stream_f64(a.F + r, pol_keep);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) g[j] = uc[c[j]];
+        u_self = (c[0] == node) ? g[0] : uc[node];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(w[j], g[j]));
+      }
+      const double value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(fk, acc)));
       un[node] = value;
       bad |= !isfinite(value);
       if (need_res) {

@@ -456,7 +456,8 @@ def test_every_width_matches_oracle(n):
 
 
 # ---- grid-resident loop (rows in every SM's shared memory) -------------------
-@pytest.mark.parametrize("target,n,m", [(20_000, 15, 2), (150_000, 15, 2), (60_000, 30, 4), (20_000, 56, 6)])
+@pytest.mark.parametrize("target,n,m", [(20_000, 15, 2), (150_000, 15, 2), (60_000, 30, 4), (20_000, 56, 6),
+                                         (400_000, 15, 2), (250_000, 30, 4)])  # last two: rows partly in L2
 def test_grid_loop_matches_oracle(synth_cache, target, n, m):
     """One cooperative launch for all steps: fixed runs of every length, swap
     and copy-back, continued runs, steady mode, and the failure step."""

@@ -8,7 +8,9 @@ import paper_2107_03632_b200 as rb  # noqa: E402
 from paper_2107_03632_b200 import synth  # noqa: E402
 
 n, m = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (15, 2)
-for target in (12_000, 20_000, 50_000, 100_000, 150_000, 200_000, 400_000):
+import os
+sizes = [int(float(x)) for x in os.environ.get('SIZES', '12000,20000,50000,100000,150000,200000,400000').split(',')]
+for target in sizes:
     nodes, st, sh = synth.synthetic_problem(target, n, m, weights="gpu")
     interior = sh.interior_nodes
     f = rb.forcing(nodes.positions[interior])
@@ -16,8 +18,7 @@ for target in (12_000, 20_000, 50_000, 100_000, 150_000, 200_000, 400_000):
     dt = 0.5 * rb.stability_bound(sh)
     steps = 4000
     out = {}
-    for name, kw in (("single", dict(pair=False, resident=False)), ("pair", dict(pair=True, resident=False)),
-                     ("grid", dict(resident=True))):
+    for name, kw in (("single", dict(pair=False, resident=False)), ("grid", dict(resident=True))):
         p = rb.Plan(nodes.n_total, interior, st.neighbors[interior], sh.weights, f, nodes.positions,
                     renumber=True, cluster=False, **kw)
         if name == "grid" and p.info()["variant"] != 4:
