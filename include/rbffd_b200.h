@@ -48,7 +48,8 @@ extern "C" {
 
 /* plan flags */
 #define RBF_RENUMBER_MORTON 0x1u  /* locality renumbering of interior rows (needs positions) */
-#define RBF_NO_RESIDENT 0x2u      /* never use the on-chip (single-CTA) resident loop */
+#define RBF_NO_RESIDENT 0x2u      /* never use an on-chip loop (single-CTA, cluster or grid-resident):
+                                     always the streaming step */
 #define RBF_NO_PDL 0x4u           /* disable programmatic dependent launch between steps */
 #define RBF_STREAM_LDG 0x8u       /* streaming step with plain loads instead of the TMA ring */
 #define RBF_NO_CLUSTER 0x10u      /* small problems: single-CTA resident loop, not the cluster loop */
