@@ -180,3 +180,50 @@ def test_gloo_world2_partitioned_loop_is_bitwise(name, steps):
     assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
     field_ok, res_ok = q.get(timeout=10)
     assert field_ok and res_ok
+
+
+def test_push_mode_blob_exchange_packing():
+    """_Group._push_ipc: every rank's export blob reaches rbf_group_push_import
+    once, in rank order, padded to a common stride (host logic only: the
+    library calls are recorded by a stand-in)."""
+    from paper_2107_03632_b200.multigpu import _Group
+
+    class FakeLib:
+        def __init__(self, blob):
+            self.blob = blob
+            self.imported = None
+
+        def rbf_group_push_export(self, h, buf, cap, n_ptr):
+            import ctypes
+
+            ctypes.memmove(buf, self.blob, len(self.blob))
+            n_ptr._obj.value = len(self.blob)
+            return 0
+
+        def rbf_group_push_import(self, h, n, flat, stride):
+            self.imported = (n, bytes(flat.raw), stride)
+            return 0
+
+    class FakePlan:
+        @staticmethod
+        def _check(rc):
+            assert rc == 0
+
+    others = [b"rank0-blob-xx", b"rank1-longer-blob!!", b"r2"]
+    g = _Group.__new__(_Group)
+    g._lib = FakeLib(others[1])
+    g._h = None
+    g.plans = [FakePlan()]
+    seen = {}
+
+    def allgather(mine):
+        seen["mine"] = mine
+        return [others[0], mine, others[2]]
+
+    g._push_ipc(allgather)
+    assert seen["mine"] == others[1]
+    n, flat, stride = g._lib.imported
+    assert n == 3 and stride == max(len(b) for b in others)
+    for k, b in enumerate(others):
+        assert flat[k * stride:k * stride + len(b)] == b
+        assert flat[k * stride + len(b):(k + 1) * stride] == b"\0" * (stride - len(b))
