@@ -50,8 +50,11 @@ PairFn pair_kernel_for(int n, int* cw);
 // B Dirichlet nodes first, stream-ordered on `st`.  Returns 0 or an RBF_ERR_*
 // code (message via rbf_detail::fail_c); *ok = false when the layout does not
 // apply (local ids would not fit 16 bits).
+// ts_fixed > 0: tiles of exactly ts_fixed slices; tables_only: build the halo /
+// local-id tables without requiring the pair kernel (the grid-resident loop's
+// two-step mode uses them).
 int pair_build(const StepArgs& a, int sps, int tiles_per_cta, int sms, size_t smem_budget,
-               cudaStream_t st, PairPlan* out, bool* ok);
+               cudaStream_t st, PairPlan* out, bool* ok, int ts_fixed = 0, bool tables_only = false);
 void pair_free(PairPlan* pp, cudaStream_t st);
 
 }  // namespace rbf

@@ -490,11 +490,12 @@ PairFn pair_kernel_for(int n, int* cw) {
   } while (0)
 
 int pair_build(const StepArgs& a, int sps, int tiles_per_cta, int sms, size_t smem_budget,
-               cudaStream_t st, PairPlan* out, bool* ok) {
+               cudaStream_t st, PairPlan* out, bool* ok, int ts_fixed, bool tables_only) {
   *ok = false;
   int cw = 0;
   PairFn fn = pair_kernel_for(a.n, &cw);
-  if (!fn || a.n_rows <= 0 || !a.C16 || !a.meta) return RBF_OK;
+  if (!tables_only && (!fn || !a.C16 || !a.meta)) return RBF_OK;
+  if (a.n_rows <= 0) return RBF_OK;
   const int n = a.n;
   const long long S = (a.n_rows + 31) >> 5;
   {  // the pair ring streams chunks of a power-of-two slice count
@@ -508,6 +509,7 @@ int pair_build(const StepArgs& a, int sps, int tiles_per_cta, int sms, size_t sm
   ts = std::max<long long>(ts, sps);
   ts = (ts + sps - 1) / sps * sps;
   ts = std::min<long long>(ts, std::max<long long>(sps, 64 / sps * sps));
+  if (ts_fixed > 0) ts = ts_fixed;  // tiles = the caller's CTA ranges (grid-resident loop)
   const int n_tiles = static_cast<int>((S + ts - 1) / ts);
   const long long total = S * n * 32;
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 32));
@@ -649,6 +651,14 @@ int pair_build(const StepArgs& a, int sps, int tiles_per_cta, int sms, size_t sm
   pp.block = 32 * (cw + 1);
   pp.grid = std::min(sms, n_tiles);
   *out = pp;
+  if (tables_only) {
+    if (over != 0 || !fits) {
+      pair_free(out, st);
+      return RBF_OK;
+    }
+    *ok = true;
+    return RBF_OK;
+  }
   if (over != 0 || !fits || stages < 2) {
     pair_free(out, st);
     return RBF_OK;

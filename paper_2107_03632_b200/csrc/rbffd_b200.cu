@@ -210,6 +210,8 @@ struct rbf_plan {
   int grid_ctas = 0, grid_spc = 0, grid_spr = 0;
   size_t grid_smem = 0;
   unsigned long long* grid_red = nullptr;  // [3][2] per-step partial slots
+  rbf::PairPlan grid_pair;                 // two steps per barrier: halo / local-id tables
+  bool grid_two = false;
   int cluster_q = 0, cluster_rpc = 0, cluster_threads = 0;
   size_t cluster_smem = 0;
   unsigned int* cluster_dest = nullptr;
@@ -770,6 +772,15 @@ int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
     a.flags = steady ? rbf::kSteady : 0;
     a.st = p->st;
     a.red = p->grid_red;
+    const rbf::PairArgs& gp = p->grid_pair.args;
+    a.HW = p->grid_two ? gp.HW : nullptr;
+    a.HC = gp.HC;
+    a.HF = gp.HF;
+    a.HR = gp.HR;
+    a.L16 = gp.L16;
+    a.hoff = gp.hoff;
+    a.hsl = gp.hsl;
+    a.u1_cap = gp.u1_cap;
     RBF_CK(cudaMemsetAsync(p->grid_red, 0, 7 * sizeof(unsigned long long), p->stream));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p->grid_ctas);
@@ -1020,8 +1031,24 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
         p->grid_fn = gfn;
         p->grid_spc = static_cast<int>(spc);
         p->grid_spr = static_cast<int>(spr);
-        p->grid_ctas = static_cast<int>((p->S + spc - 1) / spc);
         p->grid_smem = gsmem;
+        // two steps per grid barrier when every row is on chip: the pair
+        // tables with one tile per CTA (pair_kernels.cu), U1 after the rows
+        const char* gp_env = std::getenv("RBFFD_GRID_PAIR");
+        if (spr == spc && gp_env && std::atoi(gp_env) == 1) {
+          bool tok = false;
+          RBF_TRY(rbf::pair_build(p->args(), 1, 1, sms, 0, p->stream, &p->grid_pair, &tok, static_cast<int>(spc),
+                                  true));
+          const size_t u1b = static_cast<size_t>(p->grid_pair.args.u1_cap) * sizeof(double);
+          if (tok && gsmem + u1b + 2048 <= static_cast<size_t>(optin) &&
+              cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gfn, 512, gsmem + u1b) == cudaSuccess && occ >= 1) {
+            p->grid_two = true;
+            p->grid_smem = gsmem + u1b;
+          } else if (tok) {
+            rbf::pair_free(&p->grid_pair, p->stream);
+          }
+        }
+        p->grid_ctas = static_cast<int>((p->S + spc - 1) / spc);
         p->resident = true;
       }
     }
@@ -1986,6 +2013,7 @@ void rbf_plan_destroy(rbf_plan* p) {
   if (p->pair_graph) cudaGraphExecDestroy(p->pair_graph);
   cudaStream_t s = p->stream;
   if (p->pair_ok) rbf::pair_free(&p->pair, s);
+  if (p->grid_two) rbf::pair_free(&p->grid_pair, s);
   pool_free(p->W, s);
   pool_free(p->C, s);
   pool_free(p->F, s);

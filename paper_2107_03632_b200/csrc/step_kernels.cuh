@@ -2,6 +2,8 @@
 // (single-step streaming, resident, cluster loops, packing/renumbering).
 // Semantics, layout and parity rules: common.cuh.
 #pragma once
+#include <climits>
+
 #include "common.cuh"
 
 namespace rbf {
@@ -625,8 +627,19 @@ struct GridArgs {
                // from global memory, kept L2-resident (evict_last)
   int flags;   // kSteady
   DevStatus* st;
-  unsigned long long* red;  // [0..2] residual bits max per step slot, [6] the grid
-                            // barrier's arrival counter (+2^40 per non-finite CTA-step)
+  unsigned long long* red;  // [2s, 2s+1] residual bits max of barrier slot s (3 slots),
+                            // [6] the grid barrier's arrival counter (+2^40 / +2^52 per
+                            // CTA with a non-finite value in the first / second step)
+  // two steps per barrier (pair_kernels.cu tables, one tile per CTA), or HW == null:
+  // halo rows' W / ids / forcing / node, tile-local ids of every row, per-tile halo slices
+  const double* HW;
+  const int* HC;
+  const double* HF;
+  const int* HR;
+  const unsigned short* L16;
+  const int* hoff;
+  const int* hsl;
+  int u1_cap;
 };
 
 template <int NJ>
@@ -639,6 +652,7 @@ __global__ void __launch_bounds__(512, 1) grid_loop_kernel(GridArgs a) {
   double* sW = reinterpret_cast<double*>(gl_smem);
   double* sF = sW + static_cast<size_t>(a.spr) * NJ * 32;
   int* sC = reinterpret_cast<int*>(sF + static_cast<size_t>(a.spr) * 32);
+  double* sU1 = reinterpret_cast<double*>(sC + static_cast<size_t>(a.spr) * NJ * 32);  // two-step mode
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int nres = ns < a.spr ? ns : a.spr;  // slices held in shared memory
   const uint64_t pol_keep = policy_evict_last();
@@ -650,21 +664,31 @@ __global__ void __launch_bounds__(512, 1) grid_loop_kernel(GridArgs a) {
     }
     for (long long e = tid; e < static_cast<long long>(nres) * 32; e += blockDim.x) sF[e] = a.F[s0 * 32 + e];
   }
-  __shared__ unsigned long long s_max[16];
+  __shared__ unsigned long long s_max[16], s_max2[16];
   __shared__ unsigned int s_bad[16];
+  __shared__ unsigned long long s_seen;
   DevStatus* st = a.st;
   const double dt = st->dt, tol = st->tol;
   const bool steady = (a.flags & kSteady) != 0;
+  const bool two_ok = a.HW != nullptr && nres == ns;  // two-step mode needs every row on chip
+  const long long row_lo = s0 * 32;
+  const long long nt = a.n_rows - row_lo < static_cast<long long>(a.spc) * 32
+                           ? (a.n_rows > row_lo ? a.n_rows - row_lo : 0) : static_cast<long long>(a.spc) * 32;
   long long step = 0, bad_step = -1, conv_step = -1, last_res_step = -1;
   unsigned long long last_bits = 0;
+  long long it = 0;  // barriers passed
   int cur = 0;
+  constexpr unsigned long long kBad1 = 1ull << 40, kBad2 = 1ull << 52, kCount = kBad1 - 1;
   __syncthreads();
-  for (; step < a.limit; ++step) {
-    const bool need_res = steady || step == a.limit - 1;
+  while (step < a.limit) {
+    const bool two = two_ok && step + 2 <= a.limit;
+    const bool need1 = steady || (!two && step == a.limit - 1);
+    const bool need2 = two && (steady || step + 2 == a.limit);
     const double* uc = cur ? a.U1 : a.U0;
     double* un = cur ? a.U0 : a.U1;
-    bool bad = false;
-    unsigned long long dmax = 0ull;
+    bool bad1 = false, bad2 = false;
+    unsigned long long dmax1 = 0ull, dmax2 = 0ull;
+    // ---- step t -> t+1 for this CTA's rows (into shared memory in two-step mode)
     for (int k = warp; k < ns; k += nwarps) {
       const long long r = (s0 + k) * 32 + lane;
       if (r >= a.n_rows) continue;
@@ -697,70 +721,161 @@ __global__ void __launch_bounds__(512, 1) grid_loop_kernel(GridArgs a) {
         for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(w[j], g[j]));
       }
       const double value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(fk, acc)));
-      un[node] = value;
-      bad |= !isfinite(value);
-      if (need_res) {
+      if (two) sU1[r - row_lo] = value;
+      else un[node] = value;
+      bad1 |= !isfinite(value);
+      if (need1) {
         const unsigned long long b =
             static_cast<unsigned long long>(__double_as_longlong(fabs(__dsub_rn(value, u_self))));
-        dmax = b > dmax ? b : dmax;
+        dmax1 = b > dmax1 ? b : dmax1;
       }
     }
-    // CTA partials.  The non-finite flag rides on the barrier arrival (the
-    // counter's high bits count non-finite CTA-steps; the loop stops at the
-    // first, so any high bit means "this step"); the residual max goes to
-    // this step's slot, the slot two steps ahead is reset by CTA 0.
-    const unsigned int wb = __reduce_or_sync(0xffffffffu, bad ? 1u : 0u);
-    const unsigned long long wm = need_res ? warp_max_u64(dmax) : 0ull;
+    if (two) {
+      // halo rows of this CTA at step t+1 (recomputed exactly as their owners
+      // do) and the Dirichlet nodes its rows read, after its own rows in sU1
+      const long long h0 = a.hoff[blockIdx.x];
+      const int hn = a.hsl[blockIdx.x];
+      for (int h = warp; h < hn; h += nwarps) {
+        const long long e = (h0 + h) * 32 + lane;
+        const int hr = a.HR[e];
+        const long long loc = nt + h * 32 + lane;
+        if (hr >= 0) {
+          const long long eb = (h0 + h) * NJ * 32 + lane;
+          int c[NJ];
+          double w[NJ], g[NJ];
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            c[j] = a.HC[eb + 32 * j];
+            w[j] = a.HW[eb + 32 * j];
+          }
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) g[j] = uc[c[j]];
+          const double u_self = (c[0] == hr) ? g[0] : uc[hr];
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(w[j], g[j]));
+          sU1[loc] = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(a.HF[e], acc)));
+        } else if (hr != INT_MIN) {
+          sU1[loc] = uc[-(hr + 1)];
+        }
+      }
+      __syncthreads();
+      // ---- step t+1 -> t+2 for this CTA's rows, from shared memory
+      for (int k = warp; k < ns; k += nwarps) {
+        const long long r = (s0 + k) * 32 + lane;
+        if (r >= a.n_rows) continue;
+        const double* w = sW + static_cast<size_t>(k) * NJ * 32 + lane;
+        const unsigned short* l = a.L16 + (s0 + k) * NJ * 32 + lane;
+        double g[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) g[j] = sU1[l[32 * j]];
+        const double u_self = sU1[r - row_lo];
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(w[32 * j], g[j]));
+        const double value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(sF[k * 32 + lane], acc)));
+        un[a.dst_base + r] = value;
+        bad2 |= !isfinite(value);
+        if (need2) {
+          const unsigned long long b =
+              static_cast<unsigned long long>(__double_as_longlong(fabs(__dsub_rn(value, u_self))));
+          dmax2 = b > dmax2 ? b : dmax2;
+        }
+      }
+    }
+    // ---- CTA partials, then the grid barrier: the non-finite flags ride on
+    // the arrival (high bits; the loop stops at the first, so any high bit
+    // means this barrier), residual maxima go to this barrier's slot, the slot
+    // two barriers ahead is reset by CTA 0
+    const unsigned int wb = __reduce_or_sync(0xffffffffu, (bad1 ? 1u : 0u) | (bad2 ? 2u : 0u));
+    const unsigned long long wm1 = need1 ? warp_max_u64(dmax1) : 0ull;
+    const unsigned long long wm2 = need2 ? warp_max_u64(dmax2) : 0ull;
     if (lane == 0) {
       s_bad[warp] = wb;
-      s_max[warp] = wm;
+      s_max[warp] = wm1;
+      s_max2[warp] = wm2;
     }
     __syncthreads();
-    const int slot = static_cast<int>(step % 3);
-    constexpr unsigned long long kArrive = 1ull, kBad = 1ull << 40;
-    __shared__ unsigned long long s_seen;
+    const int slot = static_cast<int>(it % 3);
     if (tid == 0) {
       unsigned int cb = 0;
-      unsigned long long cm = 0ull;
+      unsigned long long cm1 = 0ull, cm2 = 0ull;
       for (int w = 0; w < nwarps; ++w) {
         cb |= s_bad[w];
-        cm = s_max[w] > cm ? s_max[w] : cm;
+        cm1 = s_max[w] > cm1 ? s_max[w] : cm1;
+        cm2 = s_max2[w] > cm2 ? s_max2[w] : cm2;
       }
-      if (need_res && cm) atomicMax(&a.red[slot], cm);
-      if (blockIdx.x == 0) a.red[(step + 1) % 3] = 0ull;
+      if (need1 && cm1) atomicMax(&a.red[slot * 2], cm1);
+      if (need2 && cm2) atomicMax(&a.red[slot * 2 + 1], cm2);
+      if (blockIdx.x == 0) {
+        const int nx = static_cast<int>((it + 1) % 3);
+        a.red[nx * 2] = 0ull;
+        a.red[nx * 2 + 1] = 0ull;
+      }
       // grid barrier on a monotonic arrival counter: the fence publishes the
       // CTA's field stores (ordered after the CTA barrier above), the acquire
       // spin orders every CTA's reads of the new field after all arrivals
       __threadfence();
-      atomicAdd(&a.red[6], kArrive + (cb ? kBad : 0ull));
-      const unsigned long long target = static_cast<unsigned long long>(step + 1) * gridDim.x;
+      atomicAdd(&a.red[6], 1ull + ((cb & 1u) ? kBad1 : 0ull) + ((cb & 2u) ? kBad2 : 0ull));
+      const unsigned long long target = static_cast<unsigned long long>(it + 1) * gridDim.x;
       unsigned long long v;
       do {
         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&a.red[6]) : "memory");
-      } while ((v & (kBad - 1)) < target);
+      } while ((v & kCount) < target);
       s_seen = v;
     }
     __syncthreads();
-    const bool gbad = (s_seen >> 40) != 0;
-    const unsigned long long gmax =
-        need_res ? *reinterpret_cast<volatile unsigned long long*>(&a.red[slot]) : 0ull;
-    cur ^= 1;
-    if (gbad) {
+    ++it;
+    const bool gbad1 = ((s_seen >> 40) & 0xfffull) != 0;
+    const bool gbad2 = (s_seen >> 52) != 0;
+    // the reference checks every step's flag before its residual (solver.py:200-217)
+    bool stop_at_first = false;  // two-step mode: stop with u^{t+1} (held in sU1)
+    if (gbad1) {
       bad_step = step;
-      break;
-    }
-    if (need_res) {
+      stop_at_first = two;
+    } else if (need1) {
+      const unsigned long long gmax = *reinterpret_cast<volatile unsigned long long*>(&a.red[slot * 2]);
       last_bits = gmax;
       last_res_step = step;
       if (steady && __ddiv_rn(__longlong_as_double(static_cast<long long>(gmax)), dt) <= tol) {
         conv_step = step;
-        ++step;
+        stop_at_first = two;
+      }
+    }
+    if (stop_at_first) {  // publish u^{t+1} of this CTA's rows in place of u^{t+2}
+      for (int k = warp; k < ns; k += nwarps) {
+        const long long r = (s0 + k) * 32 + lane;
+        if (r < a.n_rows) un[a.dst_base + r] = sU1[r - row_lo];
+      }
+    }
+    if (bad_step >= 0 || conv_step >= 0 || !two) {
+      cur ^= 1;
+      step += 1;
+      if (bad_step >= 0 || conv_step >= 0) break;
+      continue;
+    }
+    // second step of the pair
+    cur ^= 1;
+    if (gbad2) {
+      bad_step = step + 1;
+      step += 2;
+      break;
+    }
+    if (need2) {
+      const unsigned long long gmax = *reinterpret_cast<volatile unsigned long long*>(&a.red[slot * 2 + 1]);
+      last_bits = gmax;
+      last_res_step = step + 1;
+      if (steady && __ddiv_rn(__longlong_as_double(static_cast<long long>(gmax)), dt) <= tol) {
+        conv_step = step + 1;
+        step += 2;
         break;
       }
     }
+    step += 2;
   }
   // the field after the last executed step (after a failure: its u2) is in
   // buffer `cur`; publish it into both buffers
+  __syncthreads();
   const double* uf = cur ? a.U1 : a.U0;
   double* uo = cur ? a.U0 : a.U1;
   for (int k = warp; k < ns; k += nwarps) {
