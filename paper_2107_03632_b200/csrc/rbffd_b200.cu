@@ -115,9 +115,12 @@ struct KernelSet {
     }
   }
   static int cw() { return kCW; }
-  static GridFn grid() {
-    if constexpr (NJ > 0) return rbf::grid_loop_kernel<NJ>;
-    else return nullptr;
+  static GridFn grid(bool two) {
+    if constexpr (NJ > 0) return two ? rbf::grid_loop_kernel<NJ, true> : rbf::grid_loop_kernel<NJ, false>;
+    else {
+      (void)two;
+      return nullptr;
+    }
   }
 };
 
@@ -1002,11 +1005,12 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
   // grid-resident loop: every SM holds its share of the rows in shared memory
   const char* grid_env = std::getenv("RBFFD_GRID");
   if (!p->resident && !(flags & RBF_NO_RESIDENT) && N_i > 0 && !(grid_env && std::atoi(grid_env) == 0)) {
-    GridFn gfn = nullptr;
+    GridFn gfn = nullptr, gfn2 = nullptr;
     switch (n) {
 #define RBF_GCASE(K) \
   case K:            \
-    gfn = KernelSet<K>::grid(); \
+    gfn = KernelSet<K>::grid(false); \
+    gfn2 = KernelSet<K>::grid(true); \
     break;
       RBF_SPECIALISED(RBF_GCASE)
 #undef RBF_GCASE
@@ -1034,15 +1038,20 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
         p->grid_smem = gsmem;
         // two steps per grid barrier when every row is on chip: the pair
         // tables with one tile per CTA (pair_kernels.cu), U1 after the rows
+        // (measured: 1.1-1.2x up to ~1.3e6 stencil entries, where the grid
+        // barrier dominates a step; even or slower above; RBFFD_GRID_PAIR=0/1
+        // forces it off / on)
         const char* gp_env = std::getenv("RBFFD_GRID_PAIR");
-        if (spr == spc && gp_env && std::atoi(gp_env) == 1) {
+        const bool gp_want = gp_env ? std::atoi(gp_env) == 1 : N_i * static_cast<int64_t>(n) <= 1300000;
+        if (spr == spc && gp_want) {
           bool tok = false;
           RBF_TRY(rbf::pair_build(p->args(), 1, 1, sms, 0, p->stream, &p->grid_pair, &tok, static_cast<int>(spc),
                                   true));
           const size_t u1b = static_cast<size_t>(p->grid_pair.args.u1_cap) * sizeof(double);
-          if (tok && gsmem + u1b + 2048 <= static_cast<size_t>(optin) &&
-              cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gfn, 512, gsmem + u1b) == cudaSuccess && occ >= 1) {
+          if (tok && gsmem + u1b + 2048 <= static_cast<size_t>(optin) && set_max_smem(gfn2) == cudaSuccess &&
+              cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gfn2, 512, gsmem + u1b) == cudaSuccess && occ >= 1) {
             p->grid_two = true;
+            p->grid_fn = gfn2;
             p->grid_smem = gsmem + u1b;
           } else if (tok) {
             rbf::pair_free(&p->grid_pair, p->stream);

@@ -642,7 +642,7 @@ struct GridArgs {
   int u1_cap;
 };
 
-template <int NJ>
+template <int NJ, bool TWO>
 __global__ void __launch_bounds__(512, 1) grid_loop_kernel(GridArgs a) {
   extern __shared__ __align__(16) unsigned char gl_smem[];
   const long long S = (a.n_rows + 31) >> 5;
@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(512, 1) grid_loop_kernel(GridArgs a) {
   DevStatus* st = a.st;
   const double dt = st->dt, tol = st->tol;
   const bool steady = (a.flags & kSteady) != 0;
-  const bool two_ok = a.HW != nullptr && nres == ns;  // two-step mode needs every row on chip
+  const bool two_ok = TWO && a.HW != nullptr && nres == ns;  // two-step mode needs every row on chip
   const long long row_lo = s0 * 32;
   const long long nt = a.n_rows - row_lo < static_cast<long long>(a.spc) * 32
                            ? (a.n_rows > row_lo ? a.n_rows - row_lo : 0) : static_cast<long long>(a.spc) * 32;
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(512, 1) grid_loop_kernel(GridArgs a) {
         dmax1 = b > dmax1 ? b : dmax1;
       }
     }
-    if (two) {
+    if constexpr (TWO) if (two) {
       // halo rows of this CTA at step t+1 (recomputed exactly as their owners
       // do) and the Dirichlet nodes its rows read, after its own rows in sU1
       const long long h0 = a.hoff[blockIdx.x];
@@ -842,7 +842,7 @@ __global__ void __launch_bounds__(512, 1) grid_loop_kernel(GridArgs a) {
         stop_at_first = two;
       }
     }
-    if (stop_at_first) {  // publish u^{t+1} of this CTA's rows in place of u^{t+2}
+    if (TWO && stop_at_first) {  // publish u^{t+1} of this CTA's rows in place of u^{t+2}
       for (int k = warp; k < ns; k += nwarps) {
         const long long r = (s0 + k) * 32 + lane;
         if (r < a.n_rows) un[a.dst_base + r] = sU1[r - row_lo];
