@@ -34,7 +34,10 @@
 // read at C2 against 2 x 172 MB for two single steps), but the consumers are
 // latency-bound (15 warps, ~2 us per 32-row unit), so the pair only wins
 // where the per-launch grid dependency dominates -- 1.1-1.5x up to ~1e6
-// stencil entries -- and the driver enables it there by default.
+// stencil entries.  The driver builds it there, but at those sizes the
+// grid-resident loop (step_kernels.cuh) is faster still and runs instead; the
+// pair kernel runs when the on-chip loops are off (RBF_NO_RESIDENT), and its
+// halo / local-id tables drive the grid loop's two-step mode.
 //
 // Failure semantics: the epilogue flags a non-finite value anywhere in the
 // pair and the driver replays the run on the single-step path, which stops at

@@ -1099,7 +1099,8 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
     }
   }
   // two-step tile kernel for fixed-step runs (pair_kernels.cu)
-  // Measured (profiles/README.md, tools/pair_sweep.py): 1.1-1.5x faster up to
+  // (Runs only when no on-chip loop applies: the grid-resident loop wins at
+  // these sizes.)  Measured (profiles/README.md, tools/pair_sweep.py): 1.1-1.5x faster up to
   // ~1e6 stencil entries, where the per-launch grid dependency dominates;
   // even or slower above, where both are bound by the streamed bytes and the
   // pair kernel's extra phase-2 work.  RBF_PAIR / RBFFD_PAIR=1 force it on.
