@@ -1108,7 +1108,7 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
   const bool pair_force = (flags & RBF_PAIR) || (pair_env && std::atoi(pair_env) == 1);
   const bool pair_off = (flags & RBF_NO_PAIR) || (pair_env && std::atoi(pair_env) == 0);
   const bool pair_auto = N_i * static_cast<int64_t>(n) <= kPairAutoEntries;
-  if (p->tma_fn && p->index_bits == 16 && !pair_off && (pair_force || pair_auto)) {
+  if (p->tma_fn && p->index_bits == 16 && !pair_off && (pair_force || (pair_auto && !p->resident))) {
     int tpc = 4;
     if (const char* e = std::getenv("RBFFD_PAIR_TILES")) tpc = std::max(1, std::atoi(e));
     int optin = 0;

@@ -533,8 +533,9 @@ def test_pair_kernel_off_and_auto(synth_cache):
     interior = shapes.interior_nodes
     args = (nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
             rb.forcing(nodes.positions[interior]), nodes.positions)
-    assert Plan(*args, renumber=True).info()["pair"] == 1          # small: on by default
-    assert Plan(*args, renumber=True, pair=False).info()["pair"] == 0
+    assert Plan(*args, renumber=True, resident=False).info()["pair"] == 1  # small, streaming: on
+    assert Plan(*args, renumber=True).info()["pair"] == 0          # the grid-resident loop runs instead
+    assert Plan(*args, renumber=True, resident=False, pair=False).info()["pair"] == 0
     nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
     interior = shapes.interior_nodes
     big = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
