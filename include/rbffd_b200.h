@@ -278,6 +278,7 @@ int rbf_group_push_local(rbf_group* group);
 int rbf_group_push_export(rbf_group* group, void* blob_out, int64_t capacity, int64_t* length);
 int rbf_group_push_import(rbf_group* group, int32_t n_blobs, const void* blobs, int64_t stride);
 int rbf_group_push_mode(const rbf_group* group);
+int rbf_group_push_off(rbf_group* group);  /* back to pack + NCCL / copy (all ranks must agree) */
 
 void rbf_plan_destroy(rbf_plan* plan);
 const char* rbf_last_error(void);

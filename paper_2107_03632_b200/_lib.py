@@ -64,6 +64,7 @@ EXPORTED = (
     "rbf_group_push_export",
     "rbf_group_push_import",
     "rbf_group_push_mode",
+    "rbf_group_push_off",
 )
 
 
@@ -161,6 +162,7 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "rbf_group_push_export": ([vp, vp, i64, vp], i32),
         "rbf_group_push_import": ([vp, i32, vp, i64], i32),
         "rbf_group_push_mode": ([vp], i32),
+        "rbf_group_push_off": ([vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -659,6 +659,19 @@ int rbf_group_push_import(rbf_group* g, int32_t n_blobs, const void* blobs, int6
 
 int rbf_group_push_mode(const rbf_group* g) { return g && g->push ? 1 : 0; }
 
+// Back to the pack + NCCL / copy exchange (every rank must agree: used when
+// some rank could not map its neighbours).
+int rbf_group_push_off(rbf_group* g) {
+  if (!g) return fail(RBF_ERR_PARAM, "group is NULL");
+  g->push = false;
+  for (rbf_plan* p : g->parts) p->push = false;
+  if (g->fast_graph) {
+    cudaGraphExecDestroy(g->fast_graph);
+    g->fast_graph = nullptr;
+  }
+  return RBF_OK;
+}
+
 void rbf_group_destroy(rbf_group* g) {
   if (!g) return;
   cudaSetDevice(g->device);

@@ -234,11 +234,19 @@ class _Group:
         the neighbours' buffers.  The caller must barrier before running."""
         buf = ctypes.create_string_buffer(1024)
         n = ctypes.c_int64()
-        self.plans[0]._check(self._lib.rbf_group_push_export(self._h, buf, 1024, ctypes.byref(n)))
-        blobs = allgather(buf.raw[: n.value])
-        stride = max(len(b) for b in blobs)
-        flat = ctypes.create_string_buffer(b"".join(b.ljust(stride, b"\0") for b in blobs), stride * len(blobs))
-        self.plans[0]._check(self._lib.rbf_group_push_import(self._h, len(blobs), flat, stride))
+        ok = self._lib.rbf_group_push_export(self._h, buf, 1024, ctypes.byref(n)) == 0
+        blobs = allgather(buf.raw[: n.value] if ok else b"")
+        if ok and all(blobs):
+            stride = max(len(b) for b in blobs)
+            flat = ctypes.create_string_buffer(b"".join(b.ljust(stride, b"\0") for b in blobs),
+                                               stride * len(blobs))
+            ok = self._lib.rbf_group_push_import(self._h, len(blobs), flat, stride) == 0
+        else:
+            ok = False
+        # every rank must run the same exchange: push only if all ranks mapped
+        verdicts = allgather(b"1" if ok else b"0")
+        if not all(v == b"1" for v in verdicts):
+            self.plans[0]._check(self._lib.rbf_group_push_off(self._h))
 
     def run(self, dt, steps=0, mode="fixed", tol=1e-9, max_steps=1_000_000):
         from . import _lib

@@ -204,6 +204,10 @@ def test_push_mode_blob_exchange_packing():
             self.imported = (n, bytes(flat.raw), stride)
             return 0
 
+        def rbf_group_push_off(self, h):
+            self.off = True
+            return 0
+
     class FakePlan:
         @staticmethod
         def _check(rc):
@@ -217,6 +221,9 @@ def test_push_mode_blob_exchange_packing():
     seen = {}
 
     def allgather(mine):
+        if mine in (b"0", b"1"):  # the verdict round
+            seen["verdict"] = mine
+            return [b"1", mine, b"1"]
         seen["mine"] = mine
         return [others[0], mine, others[2]]
 
@@ -227,3 +234,4 @@ def test_push_mode_blob_exchange_packing():
     for k, b in enumerate(others):
         assert flat[k * stride:k * stride + len(b)] == b
         assert flat[k * stride + len(b):(k + 1) * stride] == b"\0" * (stride - len(b))
+    assert seen["verdict"] == b"1" and not getattr(g._lib, "off", False)
