@@ -714,6 +714,11 @@ def test_partitioned_push_mode_runs(synth_cache, push, P):
     want = orc.run_time_loop(nodes, shapes, steps=65)
     assert np.array_equal(field, want["field"]) and residual == want["residual"]
     assert group.push_mode == push
+    # switching a pushing group back to the copy exchange (rbf_group_push_off)
+    group.plans[0]._check(group._lib.rbf_group_push_off(group._h))
+    assert not group.push_mode
+    field, _, residual, _, _ = run_partitioned(group, nodes, shapes, cfg)
+    assert np.array_equal(field, want["field"]) and residual == want["residual"]
     group.close()
 
 
