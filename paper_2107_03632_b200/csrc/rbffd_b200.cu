@@ -368,7 +368,8 @@ Staging& staging() {
 }
 
 int staging_acquire(Staging& sg, int device) {
-  constexpr size_t kCap = size_t(64) << 20;
+  size_t kCap = size_t(16) << 20;  // 16 MB chunks pipeline the host copy with the DMA (8 / 64 MB: slower)
+  if (const char* e = std::getenv("RBFFD_STAGING_MB")) kCap = std::max<size_t>(1, std::atoll(e)) << 20;
   if (sg.cap == kCap && sg.device == device) return RBF_OK;
   for (int b = 0; b < 2; ++b) {
     if (sg.buf[b]) cudaFreeHost(sg.buf[b]);
