@@ -608,6 +608,22 @@ def test_full_size_config2_matches_oracle(synth_cache):
     assert np.array_equal(cb.field, rep.field) and cb.residual == rep.residual
 
 
+@pytest.mark.parametrize("target,n,m,steps", [(10_000_000, 30, 4, 4), (25_000_000, 56, 6, 3)],
+                         ids=["C3", "C4"])
+def test_full_size_configs_3_4_match_oracle(target, n, m, steps):
+    """BASELINE configs 3 and 4 at full size (the bench's own problems: the
+    reference's node set for seed 1, device kNN + weights): the kernels the
+    bench selects there (16-bit-id / int32-id TMA rings, Morton order) are
+    bitwise equal to the oracle over a few steps, fields and residual."""
+    nodes, _, shapes = synth.synthetic_problem(target, n, m, seed=1, weights="gpu")
+    want = orc.run_time_loop(nodes, shapes, steps=steps)
+    cfg = rb.SolveConfig(degree=m, support_size=n, nodes=target, steps=steps)
+    rep = rb.run_time_loop(cfg, nodes, shapes, cache=False)
+    assert np.array_equal(rep.field, want["field"])
+    assert rep.residual == want["residual"]
+    assert (rep.linf, rep.l2) == (want["linf"], want["l2"])
+
+
 # ---- node-partitioned loop on one device (multigpu.LocalGroup) ---------------
 @pytest.mark.parametrize("name,case,P", [
     ("crit6", "fixed100", 1), ("crit6", "fixed100", 2), ("crit6", "fixed100", 3),
