@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -380,7 +381,7 @@ def main():
             "stream_achieved": info["stream_bytes_per_step"] / per_launch / 1e9,
             "stream_frac": info["stream_bytes_per_step"] / per_launch / 1e9 / peak,
         },
-        "e2e": {"value": e2e_value, "unit": "node-updates/s",
+        "e2e": {"value": e2e_value if math.isfinite(e2e_value) else None, "unit": "node-updates/s",
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                 "what": "run_time_loop(config, nodes, shapes, cache=False) from host numpy arrays: "
                         "plan build + H2D (weights, int64 ids, forcing, field), K steps, D2H field"},
