@@ -144,7 +144,9 @@ int rbf_plan_weight_row_sum_max(rbf_plan* plan, double* out);
  * path): the packed device layout -- SELL weights and ids, forcing, 16-bit id
  * windows, renumbering maps -- written once and loaded straight back into
  * HBM, skipping validation, renumbering, packing and id compression.  A
- * loaded plan runs bit-identically to the plan that was saved.
+ * loaded plan runs bit-identically to the plan that was saved.  `path` must
+ * be a regular (seekable) file: sections move through pinned staging chunks
+ * with parallel positional reads / writes (RBF_ERR_PARAM otherwise).
  */
 int rbf_plan_save(const rbf_plan* plan, const char* path);
 int rbf_plan_load(rbf_plan** out, const char* path, int32_t device, uint32_t flags);
