@@ -1067,9 +1067,11 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
   }
   p->variant = p->grid_fn ? 4 : (p->cluster_fn ? 3 : (p->resident ? 0 : 1));
   if (tma_fn && !(flags & RBF_STREAM_LDG) && N_i > 0) {
-    // ring geometry: ~24 KB stages, as many as fit in ~200 KB of shared memory
+    // ring geometry: ~24 KB stages (~30 KB for 16-bit ids above n=20), as many
+    // as fit in ~200 KB of shared memory.  Slices per stage, measured: n=15 4 >
+    // 5 (0.4 %) > 8; n=30 3 = +9 % over 2; n=56 1 > 2 (profiles/README.md)
     const int slice = n * 32 * (8 + p->index_bits / 8) + 32 * 8 + (p->index_bits == 16 ? 16 : 0);
-    int sps = std::max(1, 24576 / slice);
+    int sps = std::max(1, (p->index_bits == 16 && n > 20 ? 30000 : 24576) / slice);
     if (const char* e = std::getenv("RBFFD_TMA_SPS")) sps = std::max(1, std::atoi(e));
     sps = std::max(rpl, (sps / rpl) * rpl);
     const int stage = sps * slice;
