@@ -54,8 +54,7 @@ extern "C" {
 #define RBF_STREAM_LDG 0x8u       /* streaming step with plain loads instead of the TMA ring */
 #define RBF_NO_CLUSTER 0x10u      /* small problems: single-CTA resident loop, not the cluster loop */
 #define RBF_NO_IDX16 0x20u        /* keep int32 node ids in the streamed step (no 16-bit windows) */
-#define RBF_FLOW 0x40u            /* opt-in: fixed-step runs in the persistent dataflow loop (measured
-                                     slower than the graph path on B200, profiles/README.md) */
+/* 0x40u: reserved (was an opt-in dataflow loop, measured slower and removed) */
 #define RBF_NO_PAIR 0x80u         /* fixed-step runs one step per launch (no two-step tile kernel) */
 #define RBF_PAIR 0x100u           /* two-step tile kernel for fixed-step runs at any size (default:
                                      only up to N_i*n = 1e6, where it is measured faster) */
@@ -206,12 +205,8 @@ typedef struct rbf_plan_info {
   int32_t grid, block;     /* streaming kernel launch geometry */
   int32_t variant;         /* 0 resident loop (1 CTA), 1 LDG streaming step, 2 TMA-ring
                               streaming step, 3 cluster-resident loop (DSMEM halo), 4 grid-resident
-                              loop (rows in every SM's shared memory, one cooperative launch);
-                              fixed-step runs of variant 2 use the persistent dataflow loop when
-                              flow == 1 */
+                              loop (rows in every SM's shared memory, one cooperative launch) */
   int32_t index_bits;      /* 32, or 16: two-window 16-bit ids streamed by the TMA step */
-  int32_t flow;            /* 1: fixed-step runs use the persistent dataflow loop */
-  int32_t flow_grid;       /* its CTAs (one per SM) */
   int64_t device_bytes;    /* device memory held by the plan */
   int64_t bytes_per_step;  /* algorithmic HBM bytes per step: N_i*(12n+24) */
   int64_t launches;        /* kernel launches issued by this plan so far */

@@ -26,7 +26,6 @@ RBF_NO_PDL = 0x4
 RBF_STREAM_LDG = 0x8
 RBF_NO_CLUSTER = 0x10
 RBF_NO_IDX16 = 0x20
-RBF_FLOW = 0x40
 RBF_NO_PAIR = 0x80
 RBF_PAIR = 0x100
 
@@ -81,8 +80,6 @@ class PlanInfo(ctypes.Structure):
         ("block", ctypes.c_int32),
         ("variant", ctypes.c_int32),
         ("index_bits", ctypes.c_int32),
-        ("flow", ctypes.c_int32),
-        ("flow_grid", ctypes.c_int32),
         ("device_bytes", ctypes.c_int64),
         ("bytes_per_step", ctypes.c_int64),
         ("launches", ctypes.c_int64),

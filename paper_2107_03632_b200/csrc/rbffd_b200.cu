@@ -18,7 +18,6 @@
 #include "step_kernels.cuh"
 #include "pair.h"
 #include "weights_kernels.cuh"
-#include "flow_kernels.cuh"
 #include "knn_kernels.cuh"
 
 #include <cub/cub.cuh>
@@ -79,7 +78,6 @@ using StreamFn = void (*)(rbf::StepArgs, const double*, double*, int);
 using TmaFn = void (*)(rbf::StepArgs, const double*, double*, int, rbf::TmaGeom);
 using ResidentFn = void (*)(rbf::ResidentArgs);
 using ClusterFn = void (*)(rbf::ClusterArgs);
-using FlowFn = void (*)(rbf::FlowArgs, rbf::TmaGeom);
 using GridFn = void (*)(rbf::GridArgs);
 
 template <int NJ>
@@ -107,14 +105,6 @@ struct KernelSet {
     }
   }
   static int rpl(int rpl_req) { return (rpl_req == 2 && NJ > 0 && NJ <= 20) ? 2 : 1; }
-  static FlowFn flow(bool idx16) {
-    if constexpr (NJ > 0) {
-      return idx16 ? rbf::step_flow_kernel<NJ, kCW, 2> : rbf::step_flow_kernel<NJ, kCW, 4>;
-    } else {
-      (void)idx16;
-      return nullptr;
-    }
-  }
   static int cw() { return kCW; }
   static GridFn grid(bool two) {
     if constexpr (NJ > 0) return two ? rbf::grid_loop_kernel<NJ, true> : rbf::grid_loop_kernel<NJ, false>;
@@ -223,13 +213,7 @@ struct rbf_plan {
   int4* meta = nullptr;            // per-slice {base0, base1, ok, 0}
   int index_bits = 32;
   int64_t overflow_slices = 0;
-  // persistent dataflow loop for fixed-step runs (flow_kernels.cuh)
-  FlowFn flow_fn = nullptr;
-  int flow_grid = 0, flow_spc = 0;
-  int* flow_flags = nullptr;
-  int* flow_dep_off = nullptr;
-  int* flow_dep = nullptr;
-  double* u_init = nullptr;        // start field kept for the exact re-run after a failure
+  double* u_init = nullptr;        // start field kept for the exact re-run after a failure (pair path)
   // two steps per launch (pair_kernels.cu): fixed-step runs of TMA plans
   rbf::PairPlan pair;
   bool pair_ok = false;
@@ -665,53 +649,6 @@ int run_pair(rbf_plan* p, int64_t limit, bool* fallback, int* final_buf) {
   return RBF_OK;
 }
 
-// Fixed-step loop in one persistent launch (flow_kernels.cuh).  Returns
-// RBF_OK with *fallback = true when a non-finite value appeared: the caller
-// then replays the run on the graph path, which stops at the exact step.
-int run_flow(rbf_plan* p, int64_t limit, bool* fallback) {
-  *fallback = false;
-  p->h_st->bad_step = std::numeric_limits<long long>::max();
-  RBF_CK(cudaMemcpyAsync(p->st, p->h_st, sizeof(rbf::DevStatus), cudaMemcpyHostToDevice, p->stream));
-  RBF_CK(cudaMemcpyAsync(p->u_init, p->U[0], sizeof(double) * p->N, cudaMemcpyDeviceToDevice, p->stream));
-  RBF_CK(cudaMemsetAsync(p->flow_flags, 0, sizeof(int) * p->flow_grid, p->stream));
-  rbf::FlowArgs fa;
-  fa.a = p->args();
-  fa.U0 = p->U[0];
-  fa.U1 = p->U[1];
-  fa.flags = p->flow_flags;
-  fa.dep_off = p->flow_dep_off;
-  fa.dep = p->flow_dep;
-  fa.steps = limit;
-  fa.spc = p->flow_spc;
-  fa.need_res_last = 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p->flow_grid);
-  cfg.blockDim = dim3(p->tma_block);
-  cfg.dynamicSmemBytes = p->tma_smem;
-  cfg.stream = p->stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: neighbour waits are safe
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  RBF_CK(cudaEventRecord(p->ev0, p->stream));
-  RBF_CK(cudaLaunchKernelEx(&cfg, p->flow_fn, fa, p->tma_geom));
-  rbf::flow_finalize_kernel<<<1, 32, 0, p->stream>>>(p->st, limit, 1);
-  RBF_CK(cudaGetLastError());
-  RBF_CK(cudaEventRecord(p->ev1, p->stream));
-  p->launches += 2;
-  RBF_CK(cudaStreamSynchronize(p->stream));
-  rbf::DevStatus s;
-  RBF_CK(cudaMemcpy(&s, p->st, sizeof(s), cudaMemcpyDeviceToHost));
-  if (s.bad_step >= 0) {
-    // restore the start field (both buffers) and let the caller replay exactly
-    RBF_CK(cudaMemcpyAsync(p->U[0], p->u_init, sizeof(double) * p->N, cudaMemcpyDeviceToDevice, p->stream));
-    RBF_CK(cudaMemcpyAsync(p->U[1], p->u_init, sizeof(double) * p->N, cudaMemcpyDeviceToDevice, p->stream));
-    *fallback = true;
-  }
-  return RBF_OK;
-}
-
 int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
   RBF_CK(cudaEventRecord(p->ev0, p->stream));
   if (limit > 0 && p->N_i > 0 && p->cluster_fn) {
@@ -877,7 +814,7 @@ int launch_assemble(const double* d_pos, const int* d_rows, long long cnt, long 
 }
 
 // Kernel / loop selection shared by rbf_plan_create and rbf_plan_load: 16-bit
-// ids, the resident / cluster loops, the TMA ring geometry, the dataflow loop.
+// ids, the resident / cluster loops, the TMA ring geometry.
 int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
   const int64_t N = p->N, N_i = p->N_i, B = p->B;
   const int n = p->n;
@@ -1067,11 +1004,12 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
   }
   p->variant = p->grid_fn ? 4 : (p->cluster_fn ? 3 : (p->resident ? 0 : 1));
   if (tma_fn && !(flags & RBF_STREAM_LDG) && N_i > 0) {
-    // ring geometry: ~24 KB stages (~30 KB for 16-bit ids above n=20), as many
+    // ring geometry: ~24 KB stages (~30 KB for 16-bit ids at n=30), as many
     // as fit in ~200 KB of shared memory.  Slices per stage, measured: n=15 4 >
-    // 5 (0.4 %) > 8; n=30 3 = +9 % over 2; n=56 1 > 2 (profiles/README.md)
+    // 5 (0.4 %) > 8; n=30 3 = +9 % over 2; n=56 1 > 2 (profiles/README.md).
+    // Only the measured widths get the larger stage.
     const int slice = n * 32 * (8 + p->index_bits / 8) + 32 * 8 + (p->index_bits == 16 ? 16 : 0);
-    int sps = std::max(1, (p->index_bits == 16 && n > 20 ? 30000 : 24576) / slice);
+    int sps = std::max(1, (p->index_bits == 16 && n == 30 ? 30000 : 24576) / slice);
     if (const char* e = std::getenv("RBFFD_TMA_SPS")) sps = std::max(1, std::atoi(e));
     sps = std::max(rpl, (sps / rpl) * rpl);
     const int stage = sps * slice;
@@ -1127,67 +1065,6 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
       if (ok) rbf::pair_free(&p->pair, p->stream);
       cudaGetLastError();
     }
-  }
-  // dataflow loop: one CTA per SM, contiguous slice ranges, neighbour waits
-  const char* flow_env = std::getenv("RBFFD_FLOW");
-  if (p->tma_fn && ((flags & RBF_FLOW) || (flow_env && std::atoi(flow_env) == 1))) {
-    FlowFn ffn = nullptr;
-    switch (n) {
-#define RBF_FCASE(K) \
-  case K:            \
-    ffn = KernelSet<K>::flow(p->index_bits == 16); \
-    break;
-      RBF_SPECIALISED(RBF_FCASE)
-#undef RBF_FCASE
-      default:
-        ffn = nullptr;
-    }
-    int occ = 0;
-    if (ffn && set_max_smem(ffn) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ffn, p->tma_block, p->tma_smem) == cudaSuccess &&
-        occ >= 1) {
-      const int G = sms;  // one CTA per SM (the ring fills the shared memory)
-      const int spc = static_cast<int>((p->S + G - 1) / G);
-      if (p->S >= 4LL * G && spc >= p->tma_geom.sps) {
-        const int words = (G + 31) / 32;
-        unsigned int* d_mat = nullptr;
-        RBF_TRY(pool_alloc(&d_mat, static_cast<size_t>(G) * words, p->stream));
-        RBF_CK(cudaMemsetAsync(d_mat, 0, sizeof(unsigned int) * G * words, p->stream));
-        const int blocks = static_cast<int>(std::min<int64_t>((N_i * n + 255) / 256, 148 * 16));
-        rbf::flow_dep_kernel<<<blocks, 256, 0, p->stream>>>(p->C, N_i, n, B, static_cast<long long>(spc) * 32,
-                                                            words, d_mat);
-        RBF_CK(cudaGetLastError());
-        std::vector<unsigned int> mat(static_cast<size_t>(G) * words);
-        RBF_CK(cudaMemcpyAsync(mat.data(), d_mat, sizeof(unsigned int) * mat.size(), cudaMemcpyDeviceToHost,
-                               p->stream));
-        RBF_CK(cudaStreamSynchronize(p->stream));
-        pool_free(d_mat, p->stream);
-        std::vector<int> off(G + 1, 0), dep;
-        int maxdeg = 0;
-        for (int b = 0; b < G; ++b) {
-          for (int c = 0; c < G; ++c)
-            if (mat[static_cast<size_t>(b) * words + (c >> 5)] & (1u << (c & 31))) dep.push_back(c);
-          off[b + 1] = static_cast<int>(dep.size());
-          maxdeg = std::max(maxdeg, off[b + 1] - off[b]);
-        }
-        if (maxdeg <= 160) {
-          RBF_TRY(dev_alloc(p.get(), &p->flow_dep_off, static_cast<size_t>(G + 1)));
-          RBF_TRY(dev_alloc(p.get(), &p->flow_dep, std::max<size_t>(1, dep.size())));
-          RBF_TRY(dev_alloc(p.get(), &p->flow_flags, static_cast<size_t>(G)));
-          RBF_TRY(dev_alloc(p.get(), &p->u_init, static_cast<size_t>(N)));
-          RBF_CK(cudaMemcpyAsync(p->flow_dep_off, off.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice,
-                                 p->stream));
-          if (!dep.empty())
-            RBF_CK(cudaMemcpyAsync(p->flow_dep, dep.data(), sizeof(int) * dep.size(), cudaMemcpyHostToDevice,
-                                   p->stream));
-          RBF_CK(cudaStreamSynchronize(p->stream));
-          p->flow_fn = ffn;
-          p->flow_grid = G;
-          p->flow_spc = spc;
-        }
-      }
-    }
-    cudaGetLastError();
   }
   if (!p->tma_fn) {
     RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p->stream_fn, kStreamBlock, 0));
@@ -1809,7 +1686,31 @@ int rbf_plan_load(rbf_plan** out, const char* path, int32_t device, uint32_t fla
     step(file_io(f, p->new_id, static_cast<size_t>(p->N) * sizeof(int), false, p->stream));
     step(file_io(f, p->row_of_k, static_cast<size_t>(p->N_i) * sizeof(long long), false, p->stream));
   }
+  // the file must end exactly here (a longer file is not what save wrote)
+  if (rc == RBF_OK && std::fgetc(f) != EOF) rc = fail(RBF_ERR_PARAM, "plan file: trailing bytes after the payload");
   std::fclose(f);
+  // payload range check on the device before any step kernel can gather with it
+  if (rc == RBF_OK && p->N_i > 0) {
+    unsigned int* d_err = nullptr;
+    step(pool_alloc(&d_err, 1, p->stream));
+    unsigned int h_err = 0;
+    auto ck = [&](cudaError_t e, const char* what) {
+      if (rc == RBF_OK && e != cudaSuccess) rc = fail(RBF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    if (rc == RBF_OK) {
+      ck(cudaMemsetAsync(d_err, 0, sizeof(unsigned int), p->stream), "memset");
+      const int blocks = static_cast<int>(std::min<int64_t>((p->S * 32 * p->n + 255) / 256, 148 * 16));
+      rbf::validate_plan_kernel<<<blocks, 256, 0, p->stream>>>(p->C, p->C16, p->meta, p->N_i, p->n, p->N,
+                                                               p->new_id, p->row_of_k, d_err);
+      ck(cudaGetLastError(), "validate_plan_kernel");
+      ck(cudaMemcpyAsync(&h_err, d_err, sizeof(h_err), cudaMemcpyDeviceToHost, p->stream), "d2h");
+      ck(cudaStreamSynchronize(p->stream), "validate plan");
+      pool_free(d_err, p->stream);
+      if (rc == RBF_OK && h_err)
+        rc = fail(RBF_ERR_PARAM, "plan file: corrupt payload (node ids / renumbering out of range, code " +
+                                     std::to_string(h_err) + ")");
+    }
+  }
   if (rc == RBF_OK) {
     RBF_CK(cudaMemsetAsync(p->U[0], 0, sizeof(double) * p->N, p->stream));
     RBF_CK(cudaMemsetAsync(p->U[1], 0, sizeof(double) * p->N, p->stream));
@@ -1895,7 +1796,7 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
   PhaseTimer timer;
   if (p->resident) {
     rc = run_resident(p, limit, steady, copy_back != 0);
-  } else if (p->pair_ok && !p->flow_fn && !steady && limit >= 2) {
+  } else if (p->pair_ok && !steady && limit >= 2) {
     bool fallback = false;
     int final_buf = 0;
     rc = run_pair(p, limit, &fallback, &final_buf);
@@ -1908,13 +1809,6 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
         RBF_CK(cudaMemcpyAsync(p->U[0], p->U[1], sizeof(double) * p->N, cudaMemcpyDeviceToDevice, p->stream));
         pair_buf = 0;
       }
-    }
-  } else if (p->flow_fn && !steady && !copy_back && limit >= 2) {
-    bool fallback = false;
-    rc = run_flow(p, limit, &fallback);
-    if (rc == RBF_OK && fallback) {
-      RBF_TRY(reset_status(p, dt, tol));
-      rc = run_streaming(p, limit, steady, false);
     }
   } else {
     rc = run_streaming(p, limit, steady, copy_back != 0);
@@ -2020,8 +1914,6 @@ int rbf_plan_get_info(const rbf_plan* p, rbf_plan_info* info) {
   info->bytes_per_step = p->N_i * (12LL * p->n + 24);
   info->launches = p->launches;
   info->index_bits = p->index_bits;
-  info->flow = p->flow_fn ? 1 : 0;
-  info->flow_grid = p->flow_grid;
   // bytes the streaming step actually moves: 16-bit ids, the per-slice window
   // bases, and int32 ids of the overflow slices
   info->pair = p->pair_ok ? 1 : 0;
@@ -2079,9 +1971,6 @@ void rbf_plan_destroy(rbf_plan* p) {
   pool_free(p->grid_red, s);
   pool_free(p->C16, s);
   pool_free(p->meta, s);
-  pool_free(p->flow_flags, s);
-  pool_free(p->flow_dep_off, s);
-  pool_free(p->flow_dep, s);
   pool_free(p->u_init, s);
   pool_free(p->halo_sendbuf, s);
   pool_free(p->st, s);

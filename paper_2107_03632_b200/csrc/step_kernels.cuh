@@ -818,11 +818,22 @@ __global__ void __launch_bounds__(512, 1) grid_loop_kernel(GridArgs a) {
       __threadfence();
       atomicAdd(&a.red[6], 1ull + ((cb & 1u) ? kBad1 : 0ull) + ((cb & 2u) ? kBad2 : 0ull));
       const unsigned long long target = static_cast<unsigned long long>(it + 1) * gridDim.x;
-      unsigned long long v;
-      do {
+      unsigned long long v, t0, t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      for (int spin = 0;; ++spin) {
         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&a.red[6]) : "memory");
-      } while ((v & kCount) < target);
-      s_seen = v;
+        if ((v & kCount) >= target) break;
+        if ((spin & 1023) == 1023) {  // all CTAs are co-resident: a 20 s wait is a fault
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          if (t - t0 > 20000000000ull) __trap();
+        }
+      }
+      // The flag bits belong to this barrier only when no CTA has arrived at
+      // the next one yet (count == target).  A count past target means some
+      // CTA already left this barrier, which it only does when this barrier
+      // was clean (a flagged barrier stops every CTA): its own next-barrier
+      // bits must not be read as this barrier's.
+      s_seen = ((v & kCount) == target) ? v : 0ull;
     }
     __syncthreads();
     ++it;
@@ -1061,6 +1072,37 @@ __global__ void scatter_rows_kernel(const double* __restrict__ f, const long lon
        k += static_cast<long long>(gridDim.x) * blockDim.x)
     F[row_of_k[k]] = f[k];
 }
+// Plan-file payload check (rbf_plan_load): every streamed node id in [0, N),
+// every 16-bit id of a fitting slice decodes to its int32 id, the renumbering
+// maps stay in range.  err bits: 1 C, 2 C16/meta, 4 new_id, 8 row_of_k.
+__global__ void validate_plan_kernel(const int* __restrict__ C, const unsigned short* __restrict__ C16,
+                                     const int4* __restrict__ meta, long long n_rows, int n, long long N,
+                                     const int* __restrict__ new_id, const long long* __restrict__ row_of_k,
+                                     unsigned int* err) {
+  const long long S = (n_rows + 31) >> 5;
+  const long long total = S * 32 * n;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  unsigned int e = 0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+    const long long sl = i / (32LL * n);
+    const int lane = static_cast<int>(i & 31);
+    if (sl * 32 + lane >= n_rows) continue;  // padding lanes are never read
+    const int c = C[i];
+    if (c < 0 || c >= N) e |= 1u;
+    if (C16) {
+      const int4 m = meta[sl];
+      if (m.z && decode_id(C16[i], m) != c) e |= 2u;
+    }
+  }
+  if (new_id)
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < N; i += stride)
+      if (new_id[i] < 0 || new_id[i] >= N) e |= 4u;
+  if (row_of_k)
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_rows; i += stride)
+      if (row_of_k[i] < 0 || row_of_k[i] >= n_rows) e |= 8u;
+  if (e) atomicOr(err, e);
+}
+
 __global__ void gather_field_kernel(const double* __restrict__ src, const int* __restrict__ new_id,
                                     long long N, double* __restrict__ dst) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < N;

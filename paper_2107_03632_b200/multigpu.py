@@ -305,9 +305,15 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def run_partitioned(group: _Group, nodes, shapes, config, u0: Optional[np.ndarray] = None):
+def run_partitioned(group: _Group, nodes, shapes, config, u0: Optional[np.ndarray] = None,
+                    reduce_max=None):
     """run_time_loop (solver.py:168-236) over a partitioned group; returns
-    (field, steps, residual, device_seconds) on every rank's assembled parts."""
+    (field, steps, residual, device_seconds) on every rank's assembled parts.
+
+    On a non-finite step the InstabilityError carries max|u2| of the failing
+    step's field (solver.py:200-206), assembled from the parts; with parts in
+    other processes ``reduce_max(float) -> float`` (a max over ranks, e.g. a
+    torch.distributed all_reduce) completes it."""
     from .solver import _AUTO_DT_SAFETY, apply_dirichlet, stability_bound
 
     u0 = apply_dirichlet(nodes, np.zeros(nodes.n_total)) if u0 is None else u0
@@ -320,7 +326,14 @@ def run_partitioned(group: _Group, nodes, shapes, config, u0: Optional[np.ndarra
     from . import _lib
 
     if rc == _lib.RBF_ERR_INSTABILITY:
-        raise InstabilityError(f"time loop unstable at step {bad}", step=bad, max_abs=None)
+        # the parts hold the failing step's u2; non-owned entries are Dirichlet
+        # values, identical to u2's (solver.py:201: max_abs = max|u2|)
+        failed = assemble_field(group.parts, locs, u0)
+        max_abs = float(np.max(np.abs(failed)))
+        if reduce_max is not None:
+            max_abs = float(reduce_max(max_abs))
+        raise InstabilityError(f"time loop unstable at step {bad} (max |u| = {max_abs})",
+                               step=bad, max_abs=max_abs)
     if rc == _lib.RBF_ERR_TIMEOUT:
         raise SteadyStateTimeout(f"no steady state after {steps} steps (residual {residual})",
                                  steps=steps, residual=residual)

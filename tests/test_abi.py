@@ -80,18 +80,77 @@ def test_plan_create_rejects_bad_interior_before_touching_cuda():
     assert rc == _lib.RBF_ERR_PARAM  # morton without positions
 
 
-def test_sass_is_native_sm100a_without_fma_in_the_update():
-    """The library carries sm_100a SASS; the 15-wide step kernel's update uses
-    separate DMUL/DADD (DFMA only appears in the residual's IEEE division)."""
+def _sass_with_lines(tmp_path):
+    """nvdisasm -g of every sm_100a cubin in the library: {kernel: [lines]}."""
     import shutil
     import subprocess
 
-    if not shutil.which("cuobjdump"):
-        pytest.skip("cuobjdump not on PATH")
-    out = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True,
-                         text=True, check=True).stdout
-    assert "sm_100a" in out
-    parts = re.split(r"\n\s+Function : ", out)
-    body = next(p for p in parts if p.startswith("_ZN3rbf18step_stream_kernelILi15E"))
-    assert len(re.findall(r"\bDMUL\b", body)) >= 16
-    assert len(re.findall(r"\bDADD\b", body)) >= 17
+    if not (shutil.which("cuobjdump") and shutil.which("nvdisasm")):
+        pytest.skip("cuobjdump / nvdisasm not on PATH")
+    subprocess.run(["cuobjdump", "-xelf", "all", str(_lib.LIB_PATH)], cwd=tmp_path, check=True,
+                   capture_output=True)
+    kernels = {}
+    for cubin in sorted(tmp_path.glob("*.sm_100a.cubin")):
+        text = subprocess.run(["nvdisasm", "-g", "-c", str(cubin)], capture_output=True, text=True,
+                              check=True).stdout
+        cur = None
+        for line in text.splitlines():
+            m = re.match(r"^\.text\.(\S+):", line)
+            if m:
+                cur = kernels.setdefault(m.group(1), [])
+            elif cur is not None:
+                cur.append(line)
+    return kernels
+
+
+UPDATE_KERNELS = ("step_tma_kernel", "step_stream_kernel", "grid_loop_kernel", "cluster_loop_kernel",
+                  "resident_loop_kernel", "pair_tma_kernel")
+
+
+def test_sass_is_native_sm100a_without_fma_in_the_update(tmp_path):
+    """Every kernel that runs the update (all widths, all loop variants, the
+    production TMA ring included) is sm_100a SASS whose only DFMAs are the
+    IEEE division of the steady residual (max|u2-u1| / dt): either on a
+    source line that calls __ddiv_rn or inside CUDA's out-of-line division
+    subroutine.  numba compiles the update to separate fmul/fadd (SURVEY.md
+    A.3); a contracted DFMA in the dot product would change bits."""
+    kernels = _sass_with_lines(tmp_path)
+    src_cache = {}
+
+    def src_line(path, no):
+        if path not in src_cache:
+            src_cache[path] = Path(path).read_text().splitlines() if Path(path).exists() else []
+        lines = src_cache[path]
+        return lines[no - 1] if 0 < no <= len(lines) else ""
+
+    checked = 0
+    for name, body in kernels.items():
+        if not any(k in name for k in UPDATE_KERNELS):
+            continue
+        checked += 1
+        where, sub = None, None
+        n_dmul = n_dadd = 0
+        for line in body:
+            m = re.match(r'^\s*//## File "([^"]+)", line (\d+)', line)
+            if m:
+                where = (m.group(1), int(m.group(2)))
+                continue
+            m = re.match(r"^(\$\S+):\s*$", line)
+            if m:
+                sub = m.group(1)
+                continue
+            if re.search(r"\bDMUL\b", line):
+                n_dmul += 1
+            if re.search(r"\bDADD\b", line):
+                n_dadd += 1
+            if re.search(r"\bDFMA\b", line):
+                if sub is not None:
+                    assert "div_rn_f64" in sub, (name, sub, line)
+                else:
+                    assert where is not None and "__ddiv_rn" in src_line(*where), (name, where, line)
+        m = re.search(r"ILi(\d+)E", name)
+        nj = int(m.group(1)) if m else 0
+        if nj > 0 and "step_tma_kernel" in name:  # unrolled chain: nj products, nj + 2 sums
+            assert n_dmul >= nj and n_dadd >= nj + 2, (name, n_dmul, n_dadd)
+    assert checked >= 24 * 4, checked
+    assert any(k.startswith("_ZN3rbf15step_tma_kernelILi15ELi15ELi1ELi2E") for k in kernels)

@@ -152,6 +152,28 @@ def test_explicit_step_matches_reference_loop(golden):
     assert np.array_equal(u1, snapshot)  # test_solver.py:126-131
 
 
+def test_plan_cache_sees_in_place_edits(golden):
+    """explicit_step caches the packed plan per ShapeStore; editing the
+    weights or stencils in place must not reuse stale device data (the
+    reference always reads the current arrays)."""
+    import copy
+
+    nodes, _, shapes0, z = golden("small")
+    shapes = copy.deepcopy(shapes0)
+    u1 = z["step_rand__u1"]
+    f = rb.forcing(nodes.positions)
+    a = rb.explicit_step(u1, shapes, f, 1e-4)
+    assert np.array_equal(a, orc.explicit_step(u1, shapes, f, 1e-4)[0])
+    shapes.weights *= 1.5  # in place: same buffer, same id(shapes)
+    b = rb.explicit_step(u1, shapes, f, 1e-4)
+    assert np.array_equal(b, orc.explicit_step(u1, shapes, f, 1e-4)[0])
+    assert not np.array_equal(a, b)
+    nb = shapes.stencils.neighbors
+    nb[shapes.interior_nodes[0], [1, 2]] = nb[shapes.interior_nodes[0], [2, 1]]
+    c = rb.explicit_step(u1, shapes, f, 1e-4)
+    assert np.array_equal(c, orc.explicit_step(u1, shapes, f, 1e-4)[0])
+
+
 def test_explicit_step_dt_zero_is_identity(golden):
     nodes, _, shapes, _ = golden("small")
     u1 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
@@ -326,15 +348,13 @@ def test_tma_and_ldg_step_variants_agree_with_oracle(synth_cache, target, n, m):
     u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
     dt = 0.5 * rb.stability_bound(shapes)
     want = orc.run_time_loop(nodes, shapes, steps=70)
-    for tma, pdl, idx16, flow in ((True, True, True, True), (True, True, False, True),
-                                  (True, True, True, False), (True, False, True, False),
-                                  (True, True, False, False), (False, True, True, True)):
+    for tma, pdl, idx16 in ((True, True, True), (True, False, True), (True, True, False),
+                            (False, True, True)):
         plan = Plan(nodes.n_total, interior, rows, shapes.weights, f_int, nodes.positions,
-                    renumber=True, tma=tma, pdl=pdl, idx16=idx16, flow=flow, resident=False)
+                    renumber=True, tma=tma, pdl=pdl, idx16=idx16, resident=False, pair=False)
         info = plan.info()
         assert info["variant"] == (2 if tma else 1)
         assert info["index_bits"] == (16 if (tma and idx16 and n <= 32) else 32)
-        assert info["flow"] == (1 if (tma and flow) else 0)
         plan.set_field(u0)
         res = plan.run(dt, steps=70)
         assert res.residual == want["residual"]
@@ -368,40 +388,18 @@ def test_tma_ring_many_laps_matches_ldg(synth_cache, target, n, m):
         assert np.array_equal(out[0][0], f) and out[0][1] == r
 
 
-def test_flow_loop_failure_replays_the_exact_step(synth_cache):
-    """The persistent dataflow loop only records that a non-finite value
-    appeared; the run is replayed on the graph path so the failing step and
-    the failing field are the reference's (solver.py:200-206)."""
-    nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
-    interior = shapes.interior_nodes
-    plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
-                rb.forcing(nodes.positions[interior]), flow=True)
-    assert plan.info()["flow"] == 1
-    dt = 40.0 * rb.stability_bound(shapes)
-    want = orc.run_time_loop(nodes, shapes, dt=dt, steps=200)
-    assert want["status"] == orc.ORC_INSTABILITY
-    plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
-    res = plan.run(dt, steps=200)
-    assert res.status == _lib.RBF_ERR_INSTABILITY and res.bad_step == want["step"]
-    got = plan.get_field()
-    assert np.array_equal(got, want["field"], equal_nan=True)
-    # and the plan keeps working after the replay
-    plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
-    res = plan.run(0.5 * rb.stability_bound(shapes), steps=77)
-    want = orc.run_time_loop(nodes, shapes, steps=77)
-    assert np.array_equal(plan.get_field(), want["field"]) and res.residual == want["residual"]
-
-
 @pytest.mark.parametrize("steps", [2, 3, 64, 65, 129])
-def test_flow_loop_step_counts(synth_cache, steps):
+def test_streaming_graph_chunk_step_counts(synth_cache, steps):
+    """Step counts either side of the 64-step graph chunk on the streaming
+    (TMA ring) path: graphs + direct tail launches, residual on the last."""
     nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
     interior = shapes.interior_nodes
     want = orc.run_time_loop(nodes, shapes, steps=steps)
     for idx16 in (True, False):
         plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
                     rb.forcing(nodes.positions[interior]), nodes.positions, renumber=True,
-                    flow=True, idx16=idx16)
-        assert plan.info()["flow"] == 1
+                    idx16=idx16, resident=False, pair=False)
+        assert plan.info()["variant"] == 2
         plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
         res = plan.run(0.5 * rb.stability_bound(shapes), steps=steps)
         assert np.array_equal(plan.get_field(), want["field"]) and res.residual == want["residual"]
@@ -582,8 +580,9 @@ def test_idx16_overflow_slices_path(synth_cache, monkeypatch):
 
 
 def test_synthetic_steady_streaming_matches_oracle(synth_cache):
-    """Steady mode through the graph-chunked streaming path; the stop step,
-    the residual and the field must equal the oracle's."""
+    """Steady mode through the graph-chunked streaming path (forced: at 30k
+    nodes the plan would pick the grid-resident loop) and through the default
+    path; the stop step, the residual and the field must equal the oracle's."""
     nodes, _, shapes = _synth(synth_cache, 30_000, 15, 2)
     cfg = rb.SolveConfig(degree=2, support_size=15, nodes=30_000, mode="steady", tol=1e-2,
                          max_steps=200_000)
@@ -593,6 +592,17 @@ def test_synthetic_steady_streaming_matches_oracle(synth_cache):
     assert rep.steps == want["steps"]
     assert rep.residual == want["residual"]
     assert np.array_equal(rep.field, want["field"])
+    interior = shapes.interior_nodes
+    for renumber in (False, True):
+        plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                    rb.forcing(nodes.positions[interior]), nodes.positions, renumber=renumber,
+                    resident=False, pair=False)
+        assert plan.info()["variant"] == 2 and plan.info()["resident"] == 0
+        plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
+        res = plan.run(0.5 * rb.stability_bound(shapes), mode="steady", tol=1e-2, max_steps=200_000)
+        assert res.steps_done == want["steps"] and res.residual == want["residual"]
+        assert np.array_equal(plan.get_field(), want["field"])
+        plan.close()
 
 
 def test_full_size_config2_matches_oracle(synth_cache):
@@ -682,6 +692,9 @@ def test_partitioned_group_instability_and_synthetic(golden, synth_cache):
     with pytest.raises(rb.InstabilityError) as ei:
         run_partitioned(group, nodes, shapes, cfg)
     assert ei.value.step == want["step"]
+    # max|u2| of the failing step, like solver.py:200-206
+    assert np.array_equal(np.float64(ei.value.max_abs), np.float64(want["max_abs"]),
+                          equal_nan=True)
     group.close()
 
     nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
@@ -724,6 +737,8 @@ def test_partitioned_push_mode_runs(synth_cache, push, P):
     with pytest.raises(rb.InstabilityError) as ei:
         run_partitioned(group, nodes, shapes, cfg)
     assert ei.value.step == want["step"]
+    assert np.array_equal(np.float64(ei.value.max_abs), np.float64(want["max_abs"]),
+                          equal_nan=True)
     # and the group keeps working (pushing) afterwards
     cfg = rb.SolveConfig(degree=2, support_size=15, nodes=200_000, steps=65)
     field, _, residual, _, _ = run_partitioned(group, nodes, shapes, cfg)
@@ -804,6 +819,28 @@ def test_plan_file_round_trip_is_bitwise(golden, synth_cache, tmp_path, which):
     trunc.write_bytes(path.read_bytes()[:200])
     with pytest.raises(rb.ParameterError):
         Plan.load(trunc)
+    # payload checks: trailing bytes, a node id out of range, a 16-bit id that
+    # does not decode to its int32 id (header 96 B, then W, C, F, C16, meta, ...)
+    raw = path.read_bytes()
+    longer = tmp_path / "longer.rbf"
+    longer.write_bytes(raw + b"\0")
+    with pytest.raises(rb.ParameterError, match="trailing"):
+        Plan.load(longer)
+    S, n = (a["N_i"] + 31) // 32, a["n"]
+    c_off = 96 + S * 32 * n * 8
+    corrupt = bytearray(raw)
+    corrupt[c_off:c_off + 4] = np.int32(a["N"] + 5).tobytes()
+    cpath = tmp_path / "corrupt.rbf"
+    cpath.write_bytes(bytes(corrupt))
+    with pytest.raises(rb.ParameterError, match="corrupt"):
+        Plan.load(cpath)
+    if a["index_bits"] == 16:
+        c16_off = c_off + S * 32 * n * 4 + S * 32 * 8
+        corrupt = bytearray(raw)
+        corrupt[c16_off:c16_off + 2] = np.uint16(np.frombuffer(raw[c16_off:c16_off + 2], np.uint16)[0] ^ 1).tobytes()
+        cpath.write_bytes(bytes(corrupt))
+        with pytest.raises(rb.ParameterError, match="corrupt"):
+            Plan.load(cpath)
 
 
 def test_device_morton_renumbering_is_the_z_order(synth_cache, tmp_path):
