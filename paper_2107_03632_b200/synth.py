@@ -79,16 +79,28 @@ def disk_nodes(target: int, seed: int = 1) -> NodeSet:
 
 
 def knn_stencils(nodes: NodeSet, n: int, workers: int = -1) -> StencilSet:
-    """Exact n nearest neighbours, self first, ties by (distance, index)."""
+    """Exact n nearest neighbours, self first, ties by (distance, index):
+    neighborhoods.py:51-94 restated (cKDTree with the reference's 8-entry
+    tie look-ahead; rows whose cutoff tie group reaches the look-ahead are
+    resolved by an exact scan)."""
     from scipy.spatial import cKDTree
 
-    tree = cKDTree(nodes.positions)
-    dist, idx = tree.query(nodes.positions, k=n, workers=workers)
-    if n == 1:
+    total = nodes.positions.shape[0]
+    positions = nodes.positions
+    tree = cKDTree(positions)
+    k_query = min(total, n + 8)  # neighborhoods.py:22 _TIE_PAD
+    dist, idx = tree.query(positions, k=k_query, workers=workers)
+    if dist.ndim == 1:
         dist, idx = dist[:, None], idx[:, None]
     order = np.lexsort((idx, dist))
+    dist = np.take_along_axis(dist, order, axis=1)
     idx = np.take_along_axis(idx, order, axis=1)
-    return StencilSet(n=n, neighbors=np.ascontiguousarray(idx, dtype=np.int64))
+    if k_query < total:
+        for i in np.flatnonzero(dist[:, n - 1] == dist[:, k_query - 1]):
+            d = positions - positions[i]
+            di = np.sqrt(d[:, 0] ** 2 + d[:, 1] ** 2)
+            idx[i, :n] = np.lexsort((np.arange(total), di))[:n]
+    return StencilSet(n=n, neighbors=np.ascontiguousarray(idx[:, :n], dtype=np.int64))
 
 
 def _weights_batch(supports: np.ndarray, expo: np.ndarray) -> np.ndarray:

@@ -164,7 +164,7 @@ def test_plan_cache_sees_in_place_edits(golden):
     f = rb.forcing(nodes.positions)
     a = rb.explicit_step(u1, shapes, f, 1e-4)
     assert np.array_equal(a, orc.explicit_step(u1, shapes, f, 1e-4)[0])
-    shapes.weights *= 1.5  # in place: same buffer, same id(shapes)
+    shapes.weights[...] *= 1.5  # in place: same buffer, same id(shapes)
     b = rb.explicit_step(u1, shapes, f, 1e-4)
     assert np.array_equal(b, orc.explicit_step(u1, shapes, f, 1e-4)[0])
     assert not np.array_equal(a, b)
