@@ -23,10 +23,12 @@
  *
  * Status codes (int return of every call):
  *     RBF_OK 0, RBF_ERR_CUDA 1, RBF_ERR_PARAM 2, RBF_ERR_INSTABILITY 4,
- *     RBF_ERR_TIMEOUT 5.
+ *     RBF_ERR_TIMEOUT 5, RBF_ERR_ILLCOND 6 (weight assembly only).
  * They map onto the reference exceptions (pkg/src/rbffd/errors.py):
  *     2 -> ParameterError (:4), 4 -> InstabilityError(step, max_abs) (:21-27),
- *     5 -> SteadyStateTimeout(steps, residual) (:30-36).
+ *     5 -> SteadyStateTimeout(steps, residual) (:30-36), 6 -> after the
+ *     caller's exact condition check of the flagged rows,
+ *     DegenerateStencilError(node_index, position) (:8-18).
  * rbf_last_error() returns a thread-local message for the last failure.
  *
  * Calls are synchronous.  A plan is not thread-safe: one plan per host thread.
@@ -45,6 +47,7 @@ extern "C" {
 #define RBF_ERR_PARAM 2
 #define RBF_ERR_INSTABILITY 4
 #define RBF_ERR_TIMEOUT 5
+#define RBF_ERR_ILLCOND 6
 
 /* plan flags */
 #define RBF_RENUMBER_MORTON 0x1u  /* locality renumbering of interior rows (needs positions) */
@@ -58,6 +61,8 @@ extern "C" {
 #define RBF_NO_PAIR 0x80u         /* fixed-step runs one step per launch (no two-step tile kernel) */
 #define RBF_PAIR 0x100u           /* two-step tile kernel for fixed-step runs at any size (default:
                                      only up to N_i*n = 1e6, where it is measured faster) */
+#define RBF_ACCEPT_ILLCOND 0x200u /* rbf_plan_create_assembled: accept row status 1 (the caller has
+                                     checked those rows' exact condition); status 2 still fails */
 
 /* run modes (SolveConfig.mode, solver.py:53) */
 #define RBF_MODE_FIXED 0
@@ -94,13 +99,24 @@ int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n,
  * saddle solve per row (Gaussian elimination with partial pivoting, one warp
  * per system), weights rescaled by 1/radius^2.  Agrees with the reference's
  * LAPACK solve to rounding (pinned by polynomial reproduction, like
- * test_weights.py:51-104), not bit for bit.  A zero pivot or non-finite
- * weight returns RBF_ERR_PARAM with *bad_row set (DegenerateStencilError,
- * weights.py:183-192).
+ * test_weights.py:51-104), not bit for bit.
+ *
+ * Condition guard (weights.py:29, :183-192, :250-258 reject a stencil whose
+ * np.linalg.cond, the 2-norm condition, exceeds COND_LIMIT = 1e14).  The
+ * saddle matrix K is symmetric, so kappa_2 <= kappa_1 <= S kappa_2 (S = n+M);
+ * from its LU factors the device estimates kappa_1 (Hager/Higham lower
+ * bound) and writes row_status[k] (optional, N_i bytes):
+ *     0  estimate <= 1e10 (typical stencils: 1e3-1e7): accepted;
+ *     1  estimate in (1e10, S*1e14]: the caller must check the exact 2-norm
+ *        condition of that row (np.linalg.cond) against 1e14;
+ *     2  zero pivot, non-finite weights, or estimate > S*1e14 (then
+ *        kappa_2 > 1e14 for certain): degenerate.
+ * Returns RBF_OK when every row has status 0; RBF_ERR_ILLCOND with *bad_row
+ * = the first flagged row otherwise (weights of status-0/1 rows are valid).
  */
 int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows, int64_t N_i,
                          int32_t n, int32_t degree, double* weights_out, int64_t* bad_row,
-                         int32_t device);
+                         uint8_t* row_status, int32_t device);
 
 /*
  * Exact k-nearest-neighbour supports on the device (
@@ -127,11 +143,15 @@ int rbf_generate_unit_disk_nodes(double h, const uint32_t* seed_key, int32_t key
 void rbf_free_host(void* p);
 
 /* rbf_plan_create with the weights assembled on the device straight into the
- * SELL layout (the host never holds them; positions are required). */
+ * SELL layout (the host never holds them; positions are required).  Same
+ * condition guard as rbf_assemble_weights: any flagged row fails the call
+ * with RBF_ERR_ILLCOND and fills row_status (optional, N_i bytes); with
+ * RBF_ACCEPT_ILLCOND in `flags` status-1 rows are accepted (the caller has
+ * checked them exactly), status-2 rows still fail. */
 int rbf_plan_create_assembled(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, int32_t degree,
                               const int64_t* interior, const int64_t* rows,
                               const double* positions, const double* f_int, int32_t device,
-                              uint32_t flags);
+                              uint32_t flags, uint8_t* row_status);
 
 /* max_k sum_j |w_kj| of the plan's weights (stability_bound = 2 / this,
  * solver.py:249-254), for plans whose weights never left the device. */

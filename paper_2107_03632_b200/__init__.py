@@ -6,7 +6,7 @@ argument meaning and exceptions, with the time loop running in the sm_100a
 CUDA library behind the C ABI of include/rbffd_b200.h.
 """
 
-from .errors import DeviceError, InstabilityError, ParameterError, SteadyStateTimeout
+from .errors import DegenerateStencilError, DeviceError, InstabilityError, ParameterError, SteadyStateTimeout
 from .problem import (
     NodeSet,
     ShapeStore,

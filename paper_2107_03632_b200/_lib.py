@@ -19,6 +19,7 @@ RBF_ERR_CUDA = 1
 RBF_ERR_PARAM = 2
 RBF_ERR_INSTABILITY = 4
 RBF_ERR_TIMEOUT = 5
+RBF_ERR_ILLCOND = 6
 
 RBF_RENUMBER_MORTON = 0x1
 RBF_NO_RESIDENT = 0x2
@@ -28,6 +29,7 @@ RBF_NO_CLUSTER = 0x10
 RBF_NO_IDX16 = 0x20
 RBF_NO_PAIR = 0x80
 RBF_PAIR = 0x100
+RBF_ACCEPT_ILLCOND = 0x200
 
 RBF_MODE_FIXED = 0
 RBF_MODE_STEADY = 1
@@ -147,8 +149,8 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "rbf_group_create": ([ctypes.POINTER(vp), i32, vp, vp, ctypes.c_char_p, i32, i32], i32),
         "rbf_group_run": ([vp, dbl, i64, i32, dbl, i64, pi64, pdbl, pi32, pi64, pdbl], i32),
         "rbf_group_destroy": ([vp], None),
-        "rbf_assemble_weights": ([vp, i64, vp, i64, i32, i32, vp, pi64, i32], i32),
-        "rbf_plan_create_assembled": ([ctypes.POINTER(vp), i64, i64, i32, i32, vp, vp, vp, vp, i32, u32], i32),
+        "rbf_assemble_weights": ([vp, i64, vp, i64, i32, i32, vp, pi64, vp, i32], i32),
+        "rbf_plan_create_assembled": ([ctypes.POINTER(vp), i64, i64, i32, i32, vp, vp, vp, vp, i32, u32, vp], i32),
         "rbf_plan_weight_row_sum_max": ([vp, pdbl], i32),
         "rbf_plan_save": ([vp, ctypes.c_char_p], i32),
         "rbf_plan_load": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, u32], i32),

@@ -790,7 +790,8 @@ int fill_monomials(int degree, rbf::WeightArgs* wa) {
 // Launch the weight assembly for `cnt` rows (device arrays); returns the
 // shared-memory size actually needed or an error.
 int launch_assemble(const double* d_pos, const int* d_rows, long long cnt, long long k0, int n,
-                    const rbf::WeightArgs& proto, double* d_w, long long* d_bad, cudaStream_t stream) {
+                    const rbf::WeightArgs& proto, double* d_w, long long* d_bad, unsigned char* d_status,
+                    unsigned long long* d_nflag, cudaStream_t stream) {
   rbf::WeightArgs wa = proto;
   wa.pos = d_pos;
   wa.rows = d_rows;
@@ -799,8 +800,10 @@ int launch_assemble(const double* d_pos, const int* d_rows, long long cnt, long 
   wa.n = n;
   wa.w_out = d_w;
   wa.bad_row = d_bad;
+  wa.status = d_status;
+  wa.n_flagged = d_nflag;
   const int S = n + wa.M;
-  const size_t per_warp = (static_cast<size_t>(S) * (S + 1) + 2 * n) * sizeof(double);
+  const size_t per_warp = rbf::assemble_smem_doubles(n, wa.M) * sizeof(double);
   int warps = static_cast<int>(std::min<size_t>(8, (200 * 1024) / per_warp));
   if (warps < 1) return fail(RBF_ERR_PARAM, "support too large for on-chip weight assembly");
   const size_t smem = per_warp * warps;
@@ -1079,7 +1082,8 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
 
 int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int64_t* interior,
                      const int64_t* rows, const double* weights, const double* f_int,
-                     const double* positions, int32_t device, uint32_t flags, int32_t degree) {
+                     const double* positions, int32_t device, uint32_t flags, int32_t degree,
+                     uint8_t* row_status = nullptr) {
   const bool assemble = degree >= 0;
   if (!out) return fail(RBF_ERR_PARAM, "out is NULL");
   *out = nullptr;
@@ -1227,14 +1231,16 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   RBF_TRY(pool_alloc(&d_err, 1, p->stream));
   RBF_CK(cudaMemsetAsync(d_err, 0, sizeof(int), p->stream));
   double* d_pos = nullptr;
-  long long* d_bad = nullptr;
+  long long* d_bad = nullptr;           // {first flagged row, flagged-row count}
+  unsigned char* d_status = nullptr;    // per reference row: 0 ok, 1 host check, 2 degenerate
   if (assemble && N_i > 0) {
     RBF_TRY(pool_alloc(&d_pos, static_cast<size_t>(2 * N), p->stream));
     RBF_CK(cudaMemcpyAsync(d_pos, positions, sizeof(double) * 2 * N, cudaMemcpyHostToDevice, p->stream));
-    RBF_TRY(pool_alloc(&d_bad, 1, p->stream));
-    const long long none = std::numeric_limits<long long>::max();
-    RBF_CK(cudaMemcpyAsync(d_bad, &none, sizeof(none), cudaMemcpyHostToDevice, p->stream));
-    RBF_CK(cudaStreamSynchronize(p->stream));  // `none` lives on this stack frame
+    RBF_TRY(pool_alloc(&d_bad, 2, p->stream));
+    RBF_TRY(pool_alloc(&d_status, static_cast<size_t>(N_i), p->stream));
+    const long long init[2] = {std::numeric_limits<long long>::max(), 0};
+    RBF_CK(cudaMemcpyAsync(d_bad, init, sizeof(init), cudaMemcpyHostToDevice, p->stream));
+    RBF_CK(cudaStreamSynchronize(p->stream));  // `init` lives on this stack frame
   }
   bool ids_ok = true;
   if (N_i > 0) {
@@ -1280,7 +1286,8 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
       RBF_CK(cudaMemcpyAsync(d_c, hc, sizeof(int32_t) * total, cudaMemcpyHostToDevice, p->stream));
       RBF_CK(cudaMemcpyAsync(d_f, hf, sizeof(double) * cnt, cudaMemcpyHostToDevice, p->stream));
       if (assemble) {  // weights computed on the device, never on the host
-        RBF_TRY(launch_assemble(d_pos, d_c, cnt, k0, n, wproto, d_w, d_bad, p->stream));
+        RBF_TRY(launch_assemble(d_pos, d_c, cnt, k0, n, wproto, d_w, d_bad, d_status,
+                                reinterpret_cast<unsigned long long*>(d_bad + 1), p->stream));
       } else {
         RBF_CK(cudaMemcpyAsync(d_w, hw, sizeof(double) * total, cudaMemcpyHostToDevice, p->stream));
       }
@@ -1299,6 +1306,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
     pool_free(d_err, p->stream);
     pool_free(d_pos, p->stream);
     pool_free(d_bad, p->stream);
+    pool_free(d_status, p->stream);
     rbf_plan_destroy(p.release());
     return fail(RBF_ERR_PARAM, "stencil node id out of range");
   }
@@ -1307,13 +1315,36 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   RBF_CK(cudaMemcpy(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
   pool_free(d_err, p->stream);
   if (d_bad) {
-    long long bad = 0;
-    RBF_CK(cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost));
+    long long hb[2] = {0, 0};
+    RBF_CK(cudaMemcpy(hb, d_bad, sizeof(hb), cudaMemcpyDeviceToHost));
+    int verdict = RBF_OK;
+    std::string msg;
+    if (hb[1] != 0) {  // flagged rows: the caller decides on the status-1 rows (exact 2-norm check)
+      std::vector<uint8_t> local;
+      uint8_t* stv = row_status;
+      if (!stv) {
+        local.resize(static_cast<size_t>(N_i));
+        stv = local.data();
+      }
+      RBF_CK(cudaMemcpy(stv, d_status, static_cast<size_t>(N_i), cudaMemcpyDeviceToHost));
+      int64_t first_deg = -1;
+      for (int64_t k = 0; k < N_i && first_deg < 0; ++k)
+        if (stv[k] == 2) first_deg = k;
+      if (!(flags & RBF_ACCEPT_ILLCOND) || first_deg >= 0) {
+        verdict = RBF_ERR_ILLCOND;
+        msg = "weight assembly flagged " + std::to_string(hb[1]) + " stencil(s), first at interior row " +
+              std::to_string(hb[0]) + (first_deg >= 0 ? " (degenerate: zero pivot, non-finite weights or "
+                                                        "condition estimate above n * 1e14)"
+                                                      : " (condition estimate above 1e10: needs the exact check)");
+      }
+    }
     pool_free(d_bad, p->stream);
+    pool_free(d_status, p->stream);
     pool_free(d_pos, p->stream);
-    if (bad != std::numeric_limits<long long>::max()) {
+    if (verdict != RBF_OK) {
+      pool_free(d_err, p->stream);
       rbf_plan_destroy(p.release());
-      return fail(RBF_ERR_PARAM, "degenerate stencil at interior row " + std::to_string(bad));
+      return fail(verdict, msg);
     }
   }
   if (h_err) {
@@ -1339,15 +1370,15 @@ int rbf_plan_create(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const int
 
 int rbf_plan_create_assembled(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, int32_t degree,
                               const int64_t* interior, const int64_t* rows, const double* positions,
-                              const double* f_int, int32_t device, uint32_t flags) {
+                              const double* f_int, int32_t device, uint32_t flags, uint8_t* row_status) {
   if (degree < 0) return fail(RBF_ERR_PARAM, "degree must be >= 0");
   return plan_create_impl(out, N, N_i, n, interior, rows, nullptr, f_int, positions, device, flags,
-                          degree);
+                          degree, row_status);
 }
 
 int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows, int64_t N_i,
                          int32_t n, int32_t degree, double* weights_out, int64_t* bad_row,
-                         int32_t device) {
+                         uint8_t* row_status, int32_t device) {
   if (!positions || (N_i > 0 && (!rows || !weights_out)) || n < 1 || N < 1)
     return fail(RBF_ERR_PARAM, "bad arguments");
   rbf::WeightArgs wproto = {};
@@ -1364,16 +1395,18 @@ int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows
   double* d_pos = nullptr;
   int* d_rows = nullptr;
   double* d_w = nullptr;
-  long long* d_bad = nullptr;
+  long long* d_bad = nullptr;  // {first flagged row, flagged-row count}
+  unsigned char* d_status = nullptr;
   const int64_t cap = std::min<int64_t>(N_i, std::max<int64_t>(1, (int64_t(1) << 24) / n));
-  const long long none = std::numeric_limits<long long>::max();
+  const long long none[2] = {std::numeric_limits<long long>::max(), 0};
   std::vector<int32_t> ids(static_cast<size_t>(cap) * n);
   int rc = RBF_OK;
   if (pool_alloc(&d_pos, static_cast<size_t>(2 * N), st) != RBF_OK ||
       pool_alloc(&d_rows, static_cast<size_t>(cap) * n, st) != RBF_OK ||
-      pool_alloc(&d_w, static_cast<size_t>(cap) * n, st) != RBF_OK || pool_alloc(&d_bad, 1, st) != RBF_OK)
+      pool_alloc(&d_w, static_cast<size_t>(cap) * n, st) != RBF_OK || pool_alloc(&d_bad, 2, st) != RBF_OK ||
+      pool_alloc(&d_status, static_cast<size_t>(N_i), st) != RBF_OK)
     rc = RBF_ERR_CUDA;
-  if (rc == RBF_OK && (cudaMemcpyAsync(d_bad, &none, sizeof(none), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+  if (rc == RBF_OK && (cudaMemcpyAsync(d_bad, none, sizeof(none), cudaMemcpyHostToDevice, st) != cudaSuccess ||
                        cudaMemcpyAsync(d_pos, positions, sizeof(double) * 2 * N, cudaMemcpyHostToDevice, st) != cudaSuccess))
     rc = fail(RBF_ERR_CUDA, "upload positions");
   for (int64_t k0 = 0; k0 < N_i && rc == RBF_OK; k0 += cap) {
@@ -1388,24 +1421,32 @@ int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows
       rc = fail(RBF_ERR_CUDA, "upload rows");
       break;
     }
-    rc = launch_assemble(d_pos, d_rows, cnt, k0, n, wproto, d_w, d_bad, st);
+    rc = launch_assemble(d_pos, d_rows, cnt, k0, n, wproto, d_w, d_bad, d_status,
+                         reinterpret_cast<unsigned long long*>(d_bad + 1), st);
     if (rc == RBF_OK && cudaMemcpyAsync(weights_out + k0 * n, d_w, sizeof(double) * cnt * n,
                                         cudaMemcpyDeviceToHost, st) != cudaSuccess)
       rc = fail(RBF_ERR_CUDA, "download weights");
   }
   if (rc == RBF_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBF_ERR_CUDA, "assembly");
-  long long bad = none;
-  if (rc == RBF_OK) cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost);
+  long long hb[2] = {none[0], 0};
+  if (rc == RBF_OK && cudaMemcpy(hb, d_bad, sizeof(hb), cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = fail(RBF_ERR_CUDA, "assembly status");
+  if (rc == RBF_OK && hb[1] != 0 && row_status &&
+      cudaMemcpy(row_status, d_status, static_cast<size_t>(N_i), cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = fail(RBF_ERR_CUDA, "assembly status");
+  if (rc == RBF_OK && hb[1] == 0 && row_status) std::memset(row_status, 0, static_cast<size_t>(N_i));
   pool_free(d_pos, st);
   pool_free(d_rows, st);
   pool_free(d_w, st);
   pool_free(d_bad, st);
+  pool_free(d_status, st);
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
   if (rc != RBF_OK) return rc;
-  if (bad != none) {
-    if (bad_row) *bad_row = bad;
-    return fail(RBF_ERR_PARAM, "degenerate stencil at interior row " + std::to_string(bad));
+  if (hb[1] != 0) {
+    if (bad_row) *bad_row = hb[0];
+    return fail(RBF_ERR_ILLCOND, "weight assembly flagged " + std::to_string(hb[1]) +
+                                     " stencil(s), first at interior row " + std::to_string(hb[0]));
   }
   return RBF_OK;
 }

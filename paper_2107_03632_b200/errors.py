@@ -41,5 +41,15 @@ class SteadyStateTimeout(*_bases("SteadyStateTimeout", RuntimeError)):
         self.residual = residual
 
 
+class DegenerateStencilError(*_bases("DegenerateStencilError", RuntimeError)):
+    """A local weight system is singular or numerically rank-deficient
+    (errors.py:8-18): carries the offending node index and its coordinates."""
+
+    def __init__(self, message, node_index=None, position=None):
+        RuntimeError.__init__(self, message)
+        self.node_index = node_index
+        self.position = position
+
+
 class DeviceError(RuntimeError):
     """A CUDA error reported by the C ABI (status RBF_ERR_CUDA)."""

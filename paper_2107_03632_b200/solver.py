@@ -30,7 +30,8 @@ from typing import Optional
 import numpy as np
 
 from . import _lib, _par
-from .errors import DeviceError, InstabilityError, ParameterError, SteadyStateTimeout
+from .errors import (DegenerateStencilError, DeviceError, InstabilityError, ParameterError,
+                     SteadyStateTimeout)
 from .problem import closed_form_solution, forcing, monomial_count, spacing_for_node_count
 
 DEFAULT_CHUNK = 1024  # solver.py:30 (CPU chunking knob; GPU geometry is internal)
@@ -221,9 +222,26 @@ class Plan:
             | (0 if pdl else _lib.RBF_NO_PDL) | (0 if tma else _lib.RBF_STREAM_LDG) \
             | _pair_flags(pair)
         handle = ctypes.c_void_p()
+        status = np.zeros(n_rows, dtype=np.uint8)
         rc = self._lib.rbf_plan_create_assembled(
             ctypes.byref(handle), int(n_total), int(n_rows), int(n), int(degree), _ptr(interior),
-            _ptr(rows), _ptr(pos), _ptr(f_int), int(device), flags)
+            _ptr(rows), _ptr(pos), _ptr(f_int), int(device), flags, _ptr(status))
+        if rc == _lib.RBF_ERR_ILLCOND:
+            # flagged stencils: the reference's exact 2-norm test on those rows
+            # (weights.py:250); all pass -> rebuild accepting them
+            from .weights import _resolve_flagged
+
+            hit = _resolve_flagged(status, lambda k: pos[rows[k]], degree)
+            if hit is not None:
+                k, cond = hit
+                node = int(interior[k])
+                x, y = pos[node]
+                raise DegenerateStencilError(
+                    f"degenerate stencil at node {node} ({x:.6g}, {y:.6g}): condition estimate {cond:.3e}",
+                    node_index=node, position=(float(x), float(y)))
+            rc = self._lib.rbf_plan_create_assembled(
+                ctypes.byref(handle), int(n_total), int(n_rows), int(n), int(degree), _ptr(interior),
+                _ptr(rows), _ptr(pos), _ptr(f_int), int(device), flags | _lib.RBF_ACCEPT_ILLCOND, None)
         self._check(rc)
         self._h = handle
         self.n_total, self.n_rows, self.n = int(n_total), int(n_rows), int(n)
