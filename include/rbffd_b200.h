@@ -83,7 +83,8 @@ typedef struct rbf_plan rbf_plan;
  *   interior   [N_i]    ShapeStore.interior_nodes (distinct node ids)
  *   rows       [N_i*n]  stencils.neighbors[interior], row-major (solver.py:182)
  *   weights    [N_i*n]  ShapeStore.weights, row-major
- *   f_int      [N_i]    forcing at interior nodes (solver.py:184)
+ *   f_int      [N_i]    forcing at interior nodes (solver.py:184); may be NULL (zero forcing,
+ *                       set later with rbf_set_forcing)
  *   positions  [N*2]    node coordinates, only read with RBF_RENUMBER_MORTON (may be NULL)
  * The caller keeps ownership of every host array.
  */
@@ -170,6 +171,12 @@ int rbf_plan_weight_row_sum_max(rbf_plan* plan, double* out);
 int rbf_plan_save(const rbf_plan* plan, const char* path);
 int rbf_plan_load(rbf_plan** out, const char* path, int32_t device, uint32_t flags);
 
+/* Page-locked host memory for the field-sized arrays of a call (forcing,
+ * start field, exact solution, result field): transfers from / to it skip
+ * the pinned staging copy every other host pointer goes through. */
+int rbf_host_alloc(int64_t bytes, void** out);
+void rbf_host_free_pinned(void* p);
+
 /* Replace the per-row forcing (explicit_step's f[interior], solver.py:156). */
 int rbf_set_forcing(rbf_plan* plan, const double* f_int);
 
@@ -180,6 +187,18 @@ int rbf_set_field(rbf_plan* plan, const double* u_host);
 /* Download the current field u[N] in original node order.  After
  * RBF_ERR_INSTABILITY this is the u2 of the failing step (solver.py:201). */
 int rbf_get_field(rbf_plan* plan, double* u_host);
+
+/*
+ * error_norms (solver.py:239-246) of the current field against `exact`
+ * (host [N], original node order, e.g. closed_form_solution(positions)):
+ *   linf = max|u - exact|, l2 = sqrt(mean((u - exact)**2))
+ * with numpy's bits: the differences and squares are elementwise IEEE, the
+ * max is order-free, and the sum follows numpy's pairwise summation tree
+ * (128-element blocks with 8 accumulators, splits at n/2 rounded down to a
+ * multiple of 8; numpy/_core/src/umath/loops_utils.h.src) -- block sums on
+ * the device, the tree above them on the host.
+ */
+int rbf_error_norms(rbf_plan* plan, const double* exact, double* linf, double* l2);
 
 /*
  * The time loop of run_time_loop (solver.py:191-225), on the device.

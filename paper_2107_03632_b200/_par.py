@@ -88,12 +88,16 @@ def error_norms(values: np.ndarray, exact: np.ndarray):
     return linf, math.sqrt(mean)
 
 
-def scaled_gather(scale: float, src: np.ndarray, idx: np.ndarray) -> np.ndarray:
+def scaled_gather(scale: float, src: np.ndarray, idx: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
     """scale * src[idx] (elementwise: numpy's bits) on the pool."""
     n = idx.shape[0]
     if n < PAR_MIN:
-        return scale * src[idx]
-    out = np.empty(n)
+        if out is None:
+            return scale * src[idx]
+        np.multiply(scale, src[idx], out=out)
+        return out
+    if out is None:
+        out = np.empty(n)
 
     def part(lo, hi):
         np.multiply(scale, src[idx[lo:hi]], out=out[lo:hi])

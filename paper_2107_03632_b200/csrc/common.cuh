@@ -373,7 +373,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 struct TmaGeom {
   int sps;     // slices per chunk (stage)
   int stages;  // ring depth
-  int contig;  // experiment: CTA b takes a contiguous range of chunks instead of b, b+G, ...
+  int contig;  // pair kernel: log2(sps); unused by the step kernel
   // each CTA's first `res` chunks are streamed with L2::evict_last: the ring
   // fill (issued before griddepcontrol.wait while the previous step drains,
   // and right after it) then comes from L2 in every step but the first, which

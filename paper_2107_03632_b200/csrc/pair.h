@@ -56,5 +56,7 @@ PairFn pair_kernel_for(int n, int* cw);
 int pair_build(const StepArgs& a, int sps, int tiles_per_cta, int sms, size_t smem_budget,
                cudaStream_t st, PairPlan* out, bool* ok, int ts_fixed = 0, bool tables_only = false);
 void pair_free(PairPlan* pp, cudaStream_t st);
+// Re-copy the halo rows' forcing from the plan's F (after rbf_set_forcing).
+int pair_refresh_forcing(PairPlan* pp, cudaStream_t st);
 
 }  // namespace rbf

@@ -670,6 +670,26 @@ int pair_build(const StepArgs& a, int sps, int tiles_per_cta, int sms, size_t sm
   return RBF_OK;
 }
 
+// HF[x] = F[row of HR[x]] for every computed halo entry: the halo rows'
+// forcing follows the plan's forcing (rbf_set_forcing).
+__global__ void pair_refresh_hf_kernel(const int* __restrict__ HR, long long count, const double* __restrict__ F,
+                                       long long B, double* __restrict__ HF) {
+  for (long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; x < count;
+       x += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c = HR[x];
+    if (c >= 0) HF[x] = F[c - B];
+  }
+}
+
+int pair_refresh_forcing(PairPlan* pp, cudaStream_t st) {
+  if (!pp->bufs[2] || pp->halo_slices == 0) return 0;
+  const long long count = pp->halo_slices * 32;
+  pair_refresh_hf_kernel<<<static_cast<int>(std::min<long long>((count + 255) / 256, 4096)), 256, 0, st>>>(
+      static_cast<const int*>(pp->bufs[3]), count, pp->args.a.F, pp->args.a.dst_base,
+      static_cast<double*>(pp->bufs[2]));
+  return ck(cudaGetLastError(), "refresh forcing");
+}
+
 void pair_free(PairPlan* pp, cudaStream_t st) {
   for (void*& b : pp->bufs) {
     if (b) cudaFreeAsync(b, st);

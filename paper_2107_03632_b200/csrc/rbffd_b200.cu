@@ -89,23 +89,26 @@ struct KernelSet {
   }
   // consumer warps: 15 (512-thread CTA, <= 128 registers) for narrow
   // stencils; 8 (<= 168 registers) for wide ones, which keep all NJ gathers in
-  // flight (measured 1 % faster at n=56 than 15 warps gathering in two halves)
+  // flight (measured 1 % faster at n=56 than 15 warps gathering in two halves).
+  // kCWide: the most consumer warps the register file holds for the widths the
+  // benchmarks use (n=15: 23 at <= 80 registers, n=30: 18 at <= 104, n=56: 11
+  // at <= 160); chosen with RBFFD_TMA_CW=<kCWide>.
   static constexpr int kCW = NJ <= 32 ? 15 : 8;
-  static TmaFn tma(int rpl_req, bool idx16) {
+  static constexpr int kCWide = NJ == 15 ? 23 : (NJ == 30 ? 18 : (NJ == 56 ? 11 : kCW));
+  static TmaFn tma(int cw_req, bool idx16) {
     if constexpr (NJ > 0) {
-      // two rows per lane measured slower on B200 (profiles/); opt-in only
-      if constexpr (NJ <= 20) {
-        if (rpl_req == 2) return rbf::step_tma_kernel<NJ, kCW, 2, 4>;
+      if constexpr (kCWide != kCW) {
+        if (cw_req == kCWide)
+          return idx16 ? rbf::step_tma_kernel<NJ, kCWide, 1, 2> : rbf::step_tma_kernel<NJ, kCWide, 1, 4>;
       }
       return idx16 ? rbf::step_tma_kernel<NJ, kCW, 1, 2> : rbf::step_tma_kernel<NJ, kCW, 1, 4>;
     } else {
-      (void)rpl_req;
+      (void)cw_req;
       (void)idx16;
       return nullptr;
     }
   }
-  static int rpl(int rpl_req) { return (rpl_req == 2 && NJ > 0 && NJ <= 20) ? 2 : 1; }
-  static int cw() { return kCW; }
+  static int cw(int cw_req) { return (NJ > 0 && cw_req == kCWide) ? kCWide : kCW; }
   static GridFn grid(bool two) {
     if constexpr (NJ > 0) return two ? rbf::grid_loop_kernel<NJ, true> : rbf::grid_loop_kernel<NJ, false>;
     else {
@@ -121,16 +124,16 @@ struct KernelSet {
   X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(12) X(15) X(16) X(20) X(21) X(24) X(28) X(30) X(32) \
   X(36) X(40) X(42) X(45) X(48) X(56) X(60) X(64)
 
-bool pick_kernels(int n, int rpl_req, bool idx16, StreamFn* s, ResidentFn* r, TmaFn* t, int* kn,
+bool pick_kernels(int n, int cw_req, bool idx16, StreamFn* s, ResidentFn* r, TmaFn* t, int* kn,
                   int* rpl, int* cw) {
   switch (n) {
 #define RBF_CASE(K)                        \
   case K:                                  \
     *s = KernelSet<K>::stream();           \
     *r = KernelSet<K>::resident();         \
-    *t = KernelSet<K>::tma(rpl_req, idx16); \
-    *rpl = KernelSet<K>::rpl(rpl_req);     \
-    *cw = KernelSet<K>::cw();              \
+    *t = KernelSet<K>::tma(cw_req, idx16); \
+    *rpl = 1;                              \
+    *cw = KernelSet<K>::cw(cw_req);        \
     *kn = K;                               \
     return true;
     RBF_SPECIALISED(RBF_CASE)
@@ -188,6 +191,11 @@ struct rbf_plan {
   double* F = nullptr;
   double* U[2] = {nullptr, nullptr};
   double* tmp = nullptr;      // N doubles for permuted field transfers
+  // error norms (rbf_error_norms): numpy's pairwise-sum blocks of [0, N)
+  std::vector<long long> norm_start;  // block starts + N
+  long long* d_norm_start = nullptr;
+  double* d_norm_sum = nullptr;       // [blocks] block sums, then [blocks] = max bits slot
+  double* norm_exact = nullptr;       // N doubles (tmp when the plan is renumbered)
   int* new_id = nullptr;      // [N] original -> plan node id; nullptr = identity
   long long* row_of_k = nullptr;  // [N_i] reference row k -> plan row; nullptr = identity
   rbf::DevStatus* st = nullptr;
@@ -379,7 +387,23 @@ int staging_acquire(Staging& sg, int device) {
 // host copy of chunk c-1, and the host copies use every core.
 constexpr size_t kFieldStagedMin = size_t(4) << 20;  // bytes; below this a plain copy is faster
 
+// Host memory already page-locked (cudaMallocHost / rbf_host_alloc /
+// registered): the DMA reads or writes it directly, no staging copy.
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 int staged_d2h(double* dst, const double* dsrc, size_t count, cudaStream_t st, int device) {
+  if (is_pinned(dst)) {
+    RBF_CK(cudaMemcpyAsync(dst, dsrc, count * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RBF_CK(cudaStreamSynchronize(st));
+    return RBF_OK;
+  }
   Staging& sg = staging();
   std::lock_guard<std::mutex> lk(sg.mu);
   RBF_TRY(staging_acquire(sg, device));
@@ -405,6 +429,11 @@ int staged_d2h(double* dst, const double* dsrc, size_t count, cudaStream_t st, i
 }
 
 int staged_h2d(double* ddst, const double* src, size_t count, cudaStream_t st, int device) {
+  if (is_pinned(src)) {
+    RBF_CK(cudaMemcpyAsync(ddst, src, count * sizeof(double), cudaMemcpyHostToDevice, st));
+    RBF_CK(cudaStreamSynchronize(st));
+    return RBF_OK;
+  }
   Staging& sg = staging();
   std::lock_guard<std::mutex> lk(sg.mu);
   RBF_TRY(staging_acquire(sg, device));
@@ -766,6 +795,17 @@ extern "C" {
 
 int rbf_version(void) { return 1; }
 
+int rbf_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return fail(RBF_ERR_PARAM, "bad arguments");
+  *out = nullptr;
+  RBF_CK(cudaMallocHost(out, static_cast<size_t>(std::max<int64_t>(bytes, 1))));
+  return RBF_OK;
+}
+
+void rbf_host_free_pinned(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 const char* rbf_last_error(void) { return g_err.c_str(); }
 
 }  // extern "C"
@@ -825,8 +865,8 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
   const size_t sell = static_cast<size_t>(p->S) * 32 * n;
   // ---- kernel selection -----------------------------------------------------
   int cw = 8;         // consumer warps of the TMA ring kernel (per width, KernelSet::kCW)
-  int rpl_req = 1;    // rows per lane of the TMA consumers (RBFFD_TMA_RPL=2: two, n <= 20)
-  if (const char* e = std::getenv("RBFFD_TMA_RPL")) rpl_req = std::atoi(e);
+  int cw_req = 0;     // RBFFD_TMA_CW=<KernelSet::kCWide>: the wide-CTA instantiation
+  if (const char* e = std::getenv("RBFFD_TMA_CW")) cw_req = std::atoi(e);
   TmaFn tma_fn = nullptr;
   int rpl = 1;
   // 16-bit two-window ids for the TMA ring (only worth it when almost every
@@ -869,9 +909,8 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
       }
     }
   }
-  pick_kernels(n, rpl_req, idx16 && rpl_req != 2, &p->stream_fn, &p->resident_fn, &tma_fn, &p->kernel_n,
-               &rpl, &cw);
-  p->index_bits = (idx16 && rpl_req != 2) ? 16 : 32;
+  pick_kernels(n, cw_req, idx16, &p->stream_fn, &p->resident_fn, &tma_fn, &p->kernel_n, &rpl, &cw);
+  p->index_bits = idx16 ? 16 : 32;
   const int64_t rows_pad = ((N_i + 31) / 32) * 32;
   const size_t smem = static_cast<size_t>(rows_pad) * n * (sizeof(double) + sizeof(int)) +
                       static_cast<size_t>(rows_pad) * sizeof(double) +
@@ -1029,7 +1068,7 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
     const size_t smem_t = 2 * 16 * sizeof(uint64_t) + static_cast<size_t>(stages) * stage;
     if (smem_t <= kResidentSmemMax && set_max_smem(tma_fn) == cudaSuccess) {
       p->tma_fn = tma_fn;
-      p->tma_geom = rbf::TmaGeom{sps, stages, std::getenv("RBFFD_TMA_CONTIG") ? 1 : 0, 0};
+      p->tma_geom = rbf::TmaGeom{sps, stages, 0, 0};
       p->tma_geom.res = (3 * stages) / 2;  // ring-fill chunks stay L2-resident (TmaGeom::res; sweep in profiles/README.md)
       if (const char* e = std::getenv("RBFFD_L2_RES_CHUNKS")) p->tma_geom.res = std::atoll(e);
       p->tma_smem = smem_t;
@@ -1091,8 +1130,8 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
     return fail(RBF_ERR_PARAM, "N must be in [1, 2^31-1]");
   if (N_i < 0 || N_i > N) return fail(RBF_ERR_PARAM, "need 0 <= N_i <= N");
   if (n < 1) return fail(RBF_ERR_PARAM, "support size n must be >= 1");
-  if (N_i > 0 && (!interior || !rows || (!weights && !assemble) || !f_int))
-    return fail(RBF_ERR_PARAM, "interior/rows/weights/f_int must be non-NULL");
+  if (N_i > 0 && (!interior || !rows || (!weights && !assemble)))
+    return fail(RBF_ERR_PARAM, "interior/rows/weights must be non-NULL");
   const bool morton = (flags & RBF_RENUMBER_MORTON) != 0;
   if ((morton || assemble) && !positions)
     return fail(RBF_ERR_PARAM, "RBF_RENUMBER_MORTON / weight assembly need positions");
@@ -1277,7 +1316,8 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
         ids_ok = false;
         break;
       }
-      std::memcpy(hf, f_int + k0, sizeof(double) * cnt);
+      if (f_int) std::memcpy(hf, f_int + k0, sizeof(double) * cnt);
+      else std::memset(hf, 0, sizeof(double) * cnt);  // forcing set later (rbf_set_forcing)
       if (!assemble) {
         const double* src_w = weights + k0 * n;
 #pragma omp parallel for schedule(static)
@@ -1769,16 +1809,19 @@ int rbf_set_forcing(rbf_plan* p, const double* f_int) {
   if (!p || (p->N_i > 0 && !f_int)) return fail(RBF_ERR_PARAM, "NULL argument");
   if (p->N_i == 0) return RBF_OK;
   RBF_CK(cudaSetDevice(p->device));
-  if (!p->renumbered) {
-    RBF_CK(cudaMemcpyAsync(p->F, f_int, sizeof(double) * p->N_i, cudaMemcpyHostToDevice, p->stream));
-    RBF_CK(cudaStreamSynchronize(p->stream));
-    return RBF_OK;
+  const bool staged = static_cast<size_t>(p->N_i) * sizeof(double) >= kFieldStagedMin;
+  double* dst = p->renumbered ? p->tmp : p->F;
+  if (staged) RBF_TRY(staged_h2d(dst, f_int, static_cast<size_t>(p->N_i), p->stream, p->device));
+  else RBF_CK(cudaMemcpyAsync(dst, f_int, sizeof(double) * p->N_i, cudaMemcpyHostToDevice, p->stream));
+  if (p->renumbered) {
+    // Renumbered: F[row_of_k[k]] = f_int[k].
+    const int blocks = static_cast<int>(std::min<int64_t>((p->N_i + 255) / 256, 148 * 16));
+    rbf::scatter_rows_kernel<<<blocks, 256, 0, p->stream>>>(p->tmp, p->row_of_k, p->N_i, p->F);
+    RBF_CK(cudaGetLastError());
   }
-  // Renumbered: F[row_of_k[k]] = f_int[k].
-  RBF_CK(cudaMemcpyAsync(p->tmp, f_int, sizeof(double) * p->N_i, cudaMemcpyHostToDevice, p->stream));
-  const int blocks = static_cast<int>(std::min<int64_t>((p->N_i + 255) / 256, 148 * 16));
-  rbf::scatter_rows_kernel<<<blocks, 256, 0, p->stream>>>(p->tmp, p->row_of_k, p->N_i, p->F);
-  RBF_CK(cudaGetLastError());
+  // the two-step tables carry a copy of the halo rows' forcing
+  if (p->pair_ok) RBF_TRY(rbf::pair_refresh_forcing(&p->pair, p->stream));
+  if (p->grid_two) RBF_TRY(rbf::pair_refresh_forcing(&p->grid_pair, p->stream));
   RBF_CK(cudaStreamSynchronize(p->stream));
   return RBF_OK;
 }
@@ -1818,6 +1861,81 @@ int rbf_get_field(rbf_plan* p, double* u) {
   if (bytes >= kFieldStagedMin) return staged_d2h(u, src, static_cast<size_t>(p->N), p->stream, p->device);
   RBF_CK(cudaMemcpyAsync(u, src, bytes, cudaMemcpyDeviceToHost, p->stream));
   RBF_CK(cudaStreamSynchronize(p->stream));
+  return RBF_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// numpy's pairwise summation tree over [lo, lo+n) (loops_utils.h.src):
+// blocks of <= 128 elements are leaves, larger ranges split at n/2 rounded
+// down to a multiple of 8.
+constexpr long long kPwBlock = 128;
+void pw_blocks(long long lo, long long n, std::vector<long long>& starts) {
+  if (n <= kPwBlock) {
+    starts.push_back(lo);
+    return;
+  }
+  long long n2 = n / 2;
+  n2 -= n2 % 8;
+  pw_blocks(lo, n2, starts);
+  pw_blocks(lo + n2, n - n2, starts);
+}
+double pw_combine(long long n, const double* sums, size_t& next) {
+  if (n <= kPwBlock) return sums[next++];
+  long long n2 = n / 2;
+  n2 -= n2 % 8;
+  const double a = pw_combine(n2, sums, next);
+  const double b = pw_combine(n - n2, sums, next);
+  return a + b;
+}
+}  // namespace
+
+extern "C" {
+
+int rbf_error_norms(rbf_plan* p, const double* exact, double* linf, double* l2) {
+  if (!p || !exact || !linf || !l2) return fail(RBF_ERR_PARAM, "NULL argument");
+  RBF_CK(cudaSetDevice(p->device));
+  const long long N = p->N;
+  if (p->norm_start.empty()) {
+    pw_blocks(0, N, p->norm_start);
+    p->norm_start.push_back(N);
+    const size_t nb = p->norm_start.size() - 1;
+    RBF_TRY(pool_alloc(&p->d_norm_start, nb + 1, p->stream));
+    RBF_TRY(pool_alloc(&p->d_norm_sum, nb + 1, p->stream));
+    RBF_CK(cudaMemcpyAsync(p->d_norm_start, p->norm_start.data(), sizeof(long long) * (nb + 1),
+                           cudaMemcpyHostToDevice, p->stream));
+    RBF_CK(cudaStreamSynchronize(p->stream));  // the host vector may be reallocated later
+  }
+  const long long nb = static_cast<long long>(p->norm_start.size()) - 1;
+  double* ex = p->tmp ? p->tmp : p->norm_exact;
+  if (!ex) {
+    RBF_TRY(pool_alloc(&p->norm_exact, static_cast<size_t>(N), p->stream));
+    ex = p->norm_exact;
+  }
+  if (static_cast<size_t>(N) * sizeof(double) >= kFieldStagedMin)
+    RBF_TRY(staged_h2d(ex, exact, static_cast<size_t>(N), p->stream, p->device));
+  else
+    RBF_CK(cudaMemcpyAsync(ex, exact, sizeof(double) * N, cudaMemcpyHostToDevice, p->stream));
+  unsigned long long* d_max = reinterpret_cast<unsigned long long*>(p->d_norm_sum + nb);
+  RBF_CK(cudaMemsetAsync(d_max, 0, sizeof(unsigned long long), p->stream));
+  const int eblocks = static_cast<int>(std::max<long long>(1, std::min<long long>((N + 255) / 256, 148 * 16)));
+  rbf::norm_diff_kernel<<<eblocks, 256, 0, p->stream>>>(p->U[p->cur], p->new_id, ex, N, d_max);
+  const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>((nb + 127) / 128, 148 * 8)));
+  rbf::norm_blocks_kernel<<<blocks, 128, 0, p->stream>>>(ex, p->d_norm_start, nb, p->d_norm_sum);
+  RBF_CK(cudaGetLastError());
+  std::vector<double> sums(static_cast<size_t>(nb) + 1);
+  RBF_CK(cudaMemcpyAsync(sums.data(), p->d_norm_sum, sizeof(double) * (nb + 1), cudaMemcpyDeviceToHost,
+                         p->stream));
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  size_t next = 0;
+  const double total = pw_combine(N, sums.data(), next);  // np.add.reduce(diff**2)
+  unsigned long long mb;
+  std::memcpy(&mb, &sums[nb], sizeof(mb));
+  double mx;
+  std::memcpy(&mx, &mb, sizeof(mx));
+  *linf = mx;                          // np.max(np.abs(diff))
+  *l2 = std::sqrt(total / static_cast<double>(N));  // math.sqrt(mean)
   return RBF_OK;
 }
 
@@ -2005,6 +2123,9 @@ void rbf_plan_destroy(rbf_plan* p) {
     pool_free(p->U[1], s);
   }
   pool_free(p->tmp, s);
+  pool_free(p->d_norm_start, s);
+  pool_free(p->d_norm_sum, s);
+  pool_free(p->norm_exact, s);
   pool_free(p->new_id, s);
   pool_free(p->row_of_k, s);
   pool_free(p->halo_send_idx, s);

@@ -74,10 +74,10 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
   const int stage_bytes = sps * tma_slice_bytes<NJ, IB>();
   const long long S = (a.n_rows + 31) >> 5;
   const long long nchunks = (S + sps - 1) / sps;
-  const long long cpc = (nchunks + gridDim.x - 1) / gridDim.x;
-  const long long my_n = g.contig
-      ? (blockIdx.x * cpc < nchunks ? (nchunks - blockIdx.x * cpc < cpc ? nchunks - blockIdx.x * cpc : cpc) : 0)
-      : (blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0);
+  // CTA b streams chunks b, b + G, b + 2G, ... (G = gridDim.x).  Ring
+  // positions and mbarrier phases are tracked with 32-bit counters advanced
+  // incrementally: no 64-bit division on the per-unit path.
+  const int my_n = blockIdx.x < nchunks ? static_cast<int>((nchunks - 1 - blockIdx.x) / gridDim.x + 1) : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -99,10 +99,8 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
-      auto issue = [&](long long i) {
-        const int s = static_cast<int>(i % stages);
-        const long long c = g.contig ? blockIdx.x * ((nchunks + gridDim.x - 1) / gridDim.x) + i
-                                     : blockIdx.x + i * gridDim.x;
+      auto issue = [&](int i, int s) {
+        const long long c = blockIdx.x + static_cast<long long>(i) * gridDim.x;
         const uint64_t pol = i < g.res ? pol_last : pol_first;
         const long long s0 = c * sps;
         const int ns = static_cast<int>(S - s0 < sps ? S - s0 : sps);
@@ -119,22 +117,29 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
         }
         bulk_g2s(dst + wbytes + cbytes, a.F + s0 * 32, fb, &full[s], pol);
         __threadfence_block();  // order the arm before the publication below
-        *reinterpret_cast<volatile int*>(&s_issued) = static_cast<int>(i + 1);
+        *reinterpret_cast<volatile int*>(&s_issued) = i + 1;
       };
-      const long long pre = my_n < stages ? my_n : stages;
-      for (long long i = 0; i < pre; ++i) issue(i);  // before the dependency wait
+      const int pre = my_n < stages ? my_n : stages;
+      for (int i = 0; i < pre; ++i) issue(i, i);  // before the dependency wait
       pdl_wait();
       const long long g0 = *reinterpret_cast<volatile long long*>(&st->step);
       const long long bs = *reinterpret_cast<volatile long long*>(&st->bad_step);
       const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
       if (!a.wait_flags && ((bs >= 0 && bs < g0) || (cs >= 0 && cs < g0))) {
-        for (long long i = 0; i < pre; ++i) mbar_wait(&full[i % stages], 0);  // drain the ring
+        for (int i = 0; i < pre; ++i) mbar_wait(&full[i], 0);  // drain the ring
         return;
       }
-      for (long long i = pre; i < my_n; ++i) {
-        const int s = static_cast<int>(i % stages);
-        mbar_wait(&empty[s], static_cast<uint32_t>(((i / stages) - 1) & 1));
-        issue(i);
+      // chunk i reuses stage i % stages once its previous occupant (chunk
+      // i - stages, empty-barrier phase (i / stages - 1) & 1) was consumed
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = pre; i < my_n; ++i) {
+        mbar_wait(&empty[s], ph);
+        issue(i, s);
+        if (++s == stages) {
+          s = 0;
+          ph ^= 1u;
+        }
       }
     } else {
       pdl_wait();
@@ -152,19 +157,20 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
     if (!a.wait_flags && ((bs >= 0 && bs < gstep) || (cs >= 0 && cs < gstep))) return;
     wait_peers(a.wait_flags, a.wait_mask, a.st, warp == 1, 32 * CW);
     const double dt = st->dt;
-    const int units_per_chunk = sps / RPL;
-    const long long total = my_n * units_per_chunk;  // consumer units of this CTA
-    for (long long q = warp - 1; q < total; q += CW) {
-      const long long i = q / units_per_chunk;
-      const int slot0 = static_cast<int>(q - i * units_per_chunk) * RPL;
-      const int s = static_cast<int>(i % stages);
+    const int upc = sps / RPL;  // consumer units per chunk
+    // this warp's units: warp-1, warp-1+CW, ... over (chunk i, unit u)
+    int i = (warp - 1) / upc, u = (warp - 1) - i * upc;
+    int s = i % stages;
+    uint32_t ph = static_cast<uint32_t>((i / stages) & 1);
+    while (i < my_n) {
+      const int slot0 = u * RPL;
       if (lane == 0) {
         while (*reinterpret_cast<volatile int*>(&s_issued) <= i) __nanosleep(64);
       }
       __syncwarp();
-      mbar_wait(&full[s], static_cast<uint32_t>((i / stages) & 1));
+      mbar_wait(&full[s], ph);
       const unsigned char* base = ring + static_cast<size_t>(s) * stage_bytes;
-      const long long slice0 = (g.contig ? blockIdx.x * cpc + i : blockIdx.x + i * gridDim.x) * sps + slot0;
+      const long long slice0 = (blockIdx.x + static_cast<long long>(i) * gridDim.x) * sps + slot0;
       {
         bool live[RPL];
         double g[RPL][NJ];
@@ -227,6 +233,15 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
       // release semantics; __syncwarp orders the other lanes' shared reads)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      u += CW;
+      while (u >= upc) {
+        u -= upc;
+        ++i;
+        if (++s == stages) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
     }
   }
   step_epilogue(st, gstep, bad, dmax, flags);
@@ -1101,6 +1116,54 @@ __global__ void validate_plan_kernel(const int* __restrict__ C, const unsigned s
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_rows; i += stride)
       if (row_of_k[i] < 0 || row_of_k[i] >= n_rows) e |= 8u;
   if (e) atomicOr(err, e);
+}
+
+// error_norms (solver.py:239-246), numpy's bits.  norm_diff_kernel: in
+// original node order d_i = u[new_id[i]] - exact[i]; sq[i] = d_i * d_i (in
+// place of exact) and max|d| as non-negative bit patterns (NaN patterns order
+// above every finite one, so a NaN wins like in np.max).
+__global__ void norm_diff_kernel(const double* __restrict__ u, const int* __restrict__ new_id, double* ex_sq,
+                                 long long N, unsigned long long* max_bits) {
+  unsigned long long m = 0ull;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < N;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double d = __dsub_rn(u[new_id ? new_id[g] : g], ex_sq[g]);
+    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(fabs(d)));
+    m = bits > m ? bits : m;
+    ex_sq[g] = __dmul_rn(d, d);
+  }
+  m = warp_max_u64(m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(max_bits, m);
+}
+
+// Block sums of numpy's pairwise summation (loops_utils.h.src pairwise_sum)
+// over [start[b], start[b+1]) (<= 128 elements): below 8 elements a serial
+// sum from 0.0, else 8 accumulators, their fixed combination, then the tail.
+__global__ void norm_blocks_kernel(const double* __restrict__ sq, const long long* __restrict__ start,
+                                   long long n_blocks, double* __restrict__ block_sum) {
+  for (long long b = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; b < n_blocks;
+       b += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double* a = sq + start[b];
+    const long long n = start[b + 1] - start[b];
+    double res;
+    if (n < 8) {
+      res = 0.0;
+      for (long long i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+    } else {
+      double r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = a[j];
+      long long i = 8;
+      for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+      }
+      res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    }
+    block_sum[b] = res;
+  }
 }
 
 __global__ void gather_field_kernel(const double* __restrict__ src, const int* __restrict__ new_id,

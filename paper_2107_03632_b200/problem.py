@@ -84,24 +84,28 @@ def _closed_form_serial(p):
     return np.sin(np.pi * p[..., 0]) * np.sin(np.pi * p[..., 1])
 
 
-def closed_form_solution(points):
+def closed_form_solution(points, out=None):
     """sin(pi x) sin(pi y) -- geometry.py:74-81.
 
     Large (N, 2) inputs are evaluated in 64 Ki-point chunks on a thread pool
     (numpy releases the GIL); the expression is elementwise, so every value
-    has the same bits as one call (tests/test_host.py checks it)."""
+    has the same bits as one call (tests/test_host.py checks it).  `out`
+    (optional, float64 [N]) receives the values."""
     p = np.asarray(points, dtype=float)
     if p.ndim != 2 or p.shape[0] < _PAR_MIN:
-        return _closed_form_serial(p)
-    out = np.empty(p.shape[0])
-    from concurrent.futures import ThreadPoolExecutor
+        if out is None:
+            return _closed_form_serial(p)
+        out[...] = _closed_form_serial(p)
+        return out
+    if out is None:
+        out = np.empty(p.shape[0])
+    from . import _par
 
     def run(lo):
         hi = min(lo + _PAR_CHUNK, p.shape[0])
         out[lo:hi] = _closed_form_serial(p[lo:hi])
 
-    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as pool:
-        list(pool.map(run, range(0, p.shape[0], _PAR_CHUNK)))
+    list(_par.pool().map(run, range(0, p.shape[0], _PAR_CHUNK)))  # the package's persistent pool
     return out
 
 

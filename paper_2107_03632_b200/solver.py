@@ -168,11 +168,11 @@ class Plan:
         interior = _as(interior, np.int64)
         weights = _as(weights, np.float64)
         rows = _as(rows, np.int64)
-        f_int = _as(f_int, np.float64)
+        f_int = None if f_int is None else _as(f_int, np.float64)  # None: zero, set later
         if weights.ndim != 2 or rows.shape != weights.shape:
             raise ParameterError("rows and weights must both be (N_i, n)")
         n_rows, n = weights.shape
-        if interior.shape != (n_rows,) or f_int.shape != (n_rows,):
+        if interior.shape != (n_rows,) or (f_int is not None and f_int.shape != (n_rows,)):
             raise ParameterError("interior and f_int must have one entry per weight row")
         flags = 0
         pos = None
@@ -308,6 +308,16 @@ class Plan:
             raise ParameterError("field length does not match the node set")
         self._check(self._lib.rbf_set_field(self._h, _ptr(u)))
 
+    def error_norms(self, exact: np.ndarray):
+        """(linf, l2) of the current field against `exact` [N] on the device,
+        with numpy's bits (solver.py:239-246; rbf_error_norms)."""
+        exact = _as(exact, np.float64)
+        if exact.shape != (self.n_total,):
+            raise ParameterError("field length does not match the node set")
+        linf, l2 = ctypes.c_double(), ctypes.c_double()
+        self._check(self._lib.rbf_error_norms(self._h, _ptr(exact), ctypes.byref(linf), ctypes.byref(l2)))
+        return linf.value, l2.value
+
     def get_field(self, out: Optional[np.ndarray] = None) -> np.ndarray:
         if out is None:
             out = np.empty(self.n_total, dtype=np.float64)
@@ -376,8 +386,11 @@ def _fingerprint(*arrays) -> bytes:
     return h.digest()
 
 
-def _plan_for(shapes, n_total: int, f_int: np.ndarray, positions=None, *, cache: bool = True,
+def _plan_for(shapes, n_total: int, f_int: Optional[np.ndarray], positions=None, *, cache: bool = True,
               renumber: bool = False) -> Plan:
+    """The packed plan for `shapes` (cached per ShapeStore when `cache`).
+    f_int=None leaves the forcing to a later set_forcing (a cache hit keeps
+    the previous one)."""
     weights = shapes.weights
     neighbors = shapes.stencils.neighbors
     interior = shapes.interior_nodes
@@ -388,7 +401,8 @@ def _plan_for(shapes, n_total: int, f_int: np.ndarray, positions=None, *, cache:
         hit = _PLANS.get(key)
         if hit is not None and hit[0]() is shapes and hit[2] == fp:
             plan = hit[1]
-            plan.set_forcing(f_int)
+            if f_int is not None:
+                plan.set_forcing(f_int)
             return plan
         if hit is not None:  # stale (arrays edited in place): drop the old plan
             _PLANS.pop(key, None)
@@ -409,16 +423,19 @@ def _interior_rows(neighbors: np.ndarray, interior: np.ndarray) -> np.ndarray:
     interior is the contiguous tail [B, N) as in generated node sets."""
     n_i = interior.size
     B = neighbors.shape[0] - n_i
+    # strictly increasing, n_i entries, from B to N-1: exactly the range [B, N)
     if n_i and interior[0] == B and interior[-1] == neighbors.shape[0] - 1 and \
-            np.array_equal(interior, np.arange(B, B + n_i)):
+            bool(np.all(interior[1:] > interior[:-1])):
         return np.ascontiguousarray(neighbors[B:])
     return np.ascontiguousarray(neighbors[interior])
 
 
 def clear_plan_cache() -> None:
+    """Release cached plans (HBM) and the page-locked scratch arrays."""
     for _ref, plan, _fp in list(_PLANS.values()):
         plan.close()
     _PLANS.clear()
+    _PINNED.clear()
 
 
 # ---------------------------------------------------------------------------
@@ -481,32 +498,59 @@ def run_time_loop(config: SolveConfig, nodes, shapes, copy_back: bool = False, *
     boundary; only the step loop is timed (``wall_time_s``).  Keyword-only
     extras: ``cache=True`` keeps the packed plan for these shapes alive in HBM
     for the next call (default off, like the reference, which has no cache;
-    a hit also needs the arrays' sampled fingerprint to match); ``renumber`` applies the Morton locality renumbering (bit-identical;
-    default: on from RENUMBER_MIN_ROWS interior rows).
+    a hit also needs the arrays' sampled fingerprint to match); ``renumber``
+    applies the Morton locality renumbering (bit-identical; default: on from
+    RENUMBER_MIN_ROWS interior rows).
+
+    The one-shot path overlaps its host work with the device: the plan is
+    packed and uploaded (C++, GIL released) on a helper thread while this
+    thread evaluates the closed form, forcing and Dirichlet values; the error
+    norms run on the device (rbf_error_norms, numpy's bits).
     """
     if renumber is None:
         renumber = shapes.n_rows >= RENUMBER_MIN_ROWS
     tick = _Ticker()
     interior = shapes.interior_nodes
-    # sin(pi x) sin(pi y) is evaluated once for the forcing (geometry.py:84-86),
-    # the Dirichlet values (solver.py:130-138) and the error norms
-    # (solver.py:239-246): elementwise, so each use gets the reference's bits
-    exact = closed_form_solution(nodes.positions)
-    f_int = _par.scaled_gather(2.0 * np.pi**2, exact, np.asarray(interior))  # solver.py:184
-    u1 = np.zeros(nodes.n_total)  # solver.py:186
-    bidx = nodes.boundary_indices
-    u1[bidx] = exact[bidx]
-    tick("host prep (closed form, forcing, Dirichlet)")
-    dt = config.dt if config.dt is not None else _AUTO_DT_SAFETY * stability_bound(shapes)
-    plan = _plan_for(shapes, nodes.n_total, f_int, nodes.positions if renumber else None,
-                     cache=cache, renumber=renumber)
-    tick("plan")
+    N = nodes.n_total
+    positions = nodes.positions if renumber else None
+    build = _builder().submit(_plan_for, shapes, N, None, positions, cache=cache, renumber=renumber)
+    pinned = _PINNED.acquire(N, interior.size)  # page-locked scratch, or None
+    try:
+        # sin(pi x) sin(pi y) is evaluated once for the forcing (geometry.py:84-86),
+        # the Dirichlet values (solver.py:130-138) and the error norms
+        # (solver.py:239-246): elementwise, so each use gets the reference's bits
+        exact = closed_form_solution(nodes.positions, out=None if pinned is None else pinned["exact"])
+        f_int = _par.scaled_gather(2.0 * np.pi**2, exact, np.asarray(interior),
+                                   out=None if pinned is None else pinned["f_int"])  # solver.py:184
+        if pinned is None:
+            u1 = np.zeros(N)  # solver.py:186
+        else:
+            u1 = pinned["u1"]
+            u1.fill(0.0)
+        bidx = nodes.boundary_indices
+        u1[bidx] = exact[bidx]
+        dt = config.dt if config.dt is not None else _AUTO_DT_SAFETY * stability_bound(shapes)
+        tick("host prep (closed form, forcing, Dirichlet, dt)")
+        plan = build.result()
+        tick("plan (overlapped with the host prep)")
+        return _run_planned(plan, config, shapes, copy_back, cache, dt, exact, f_int, u1, tick)
+    finally:
+        if not build.done():
+            build.result()
+        _PINNED.release(pinned)
+
+
+def _run_planned(plan, config, shapes, copy_back, cache, dt, exact, f_int, u1, tick) -> SolveReport:
+    """run_time_loop after the plan exists: forcing, field, loop, norms, field."""
+    plan.set_forcing(f_int)
     plan.set_field(u1)
     res = plan.run(dt, steps=config.steps, mode=config.mode, tol=config.tol,
                    max_steps=config.max_steps, copy_back=copy_back)
-    tick("set_field + run")
+    tick("set_forcing + set_field + run")
     if res.status == _lib.RBF_ERR_INSTABILITY:
         u2 = plan.get_field()
+        if not cache:
+            plan.close()
         max_abs = float(np.max(np.abs(u2)))
         raise InstabilityError(
             f"time loop unstable at step {res.bad_step} (max |u| = {max_abs})",
@@ -514,18 +558,20 @@ def run_time_loop(config: SolveConfig, nodes, shapes, copy_back: bool = False, *
             max_abs=max_abs,
         )
     if res.status == _lib.RBF_ERR_TIMEOUT:
+        if not cache:
+            plan.close()
         raise SteadyStateTimeout(
             f"no steady state after {res.steps_done} steps (residual {res.residual})",
             steps=res.steps_done,
             residual=res.residual,
         )
+    linf, l2 = plan.error_norms(exact)  # solver.py:227, on the device
+    tick("norms (device)")
     field_ = plan.get_field()
     tick("get_field")
     if not cache:
         plan.close()
     tick("plan close")
-    linf, l2 = _norms(field_, exact)
-    tick("norms")
     return SolveReport(
         field=field_,
         steps=res.steps_done,
@@ -536,6 +582,70 @@ def run_time_loop(config: SolveConfig, nodes, shapes, copy_back: bool = False, *
         config=config.as_dict(dt_effective=dt),
         device_seconds=res.device_seconds,
     )
+
+
+class _PinnedScratch:
+    """Page-locked host arrays for one run_time_loop call at a time (exact
+    solution, forcing, start field), kept across calls: their uploads are
+    plain DMAs instead of a staging copy.  Fields above 1 GiB, or a second
+    concurrent caller, get ordinary arrays."""
+
+    MAX_BYTES = 1 << 30
+
+    def __init__(self):
+        import threading
+
+        self._lock = threading.Lock()
+        self._bufs = {}
+
+    def _array(self, name, n):
+        ent = self._bufs.get(name)
+        if ent is None or ent[1] < n:
+            if ent is not None:
+                _lib.load().rbf_host_free_pinned(ent[0])
+                del self._bufs[name]
+            lib = _lib.load()
+            ptr = ctypes.c_void_p()
+            if lib.rbf_host_alloc(int(max(n, 1) * 8), ctypes.byref(ptr)) != _lib.RBF_OK:
+                return None
+            buf = (ctypes.c_double * max(n, 1)).from_address(ptr.value)
+            ent = (ptr, max(n, 1), np.frombuffer(buf, dtype=np.float64))
+            self._bufs[name] = ent
+        return ent[2][:n]
+
+    def acquire(self, n_total: int, n_rows: int):
+        if n_total * 8 > self.MAX_BYTES or not self._lock.acquire(blocking=False):
+            return None
+        out = {"exact": self._array("exact", n_total), "f_int": self._array("f_int", n_rows),
+               "u1": self._array("u1", n_total)}
+        if any(v is None for v in out.values()):
+            self._lock.release()
+            return None
+        return out
+
+    def release(self, handle) -> None:
+        if handle is not None:
+            self._lock.release()
+
+    def clear(self) -> None:
+        with self._lock:
+            for ptr, _, _ in self._bufs.values():
+                _lib.load().rbf_host_free_pinned(ptr)
+            self._bufs.clear()
+
+
+_PINNED = _PinnedScratch()
+_BUILDER = None
+
+
+def _builder():
+    """One helper thread for plan construction (ctypes releases the GIL)."""
+    global _BUILDER
+    if _BUILDER is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _BUILDER = ThreadPoolExecutor(max_workers=1, thread_name_prefix="rbffd-plan")
+    return _BUILDER
 
 
 class _Ticker:
@@ -556,11 +666,6 @@ class _Ticker:
             self.t = t
 
 
-def _norms(values: np.ndarray, exact: np.ndarray):
-    # max|u-u*| and sqrt(mean((u-u*)**2)) on all cores, numpy's bits (_par.py)
-    return _par.error_norms(values, exact)
-
-
 def error_norms(values: np.ndarray, nodes):
     """(linf, l2) of values minus the analytic solution over all nodes (solver.py:239-246)."""
     if len(values) != nodes.n_total:
@@ -572,8 +677,14 @@ def stability_bound(shapes) -> float:
     """2 / max_k sum_j |w_kj| (solver.py:249-254)."""
     if shapes.n_rows == 0:
         raise ParameterError("empty shape store")
-    row_sums = np.abs(shapes.weights).sum(axis=1)
-    return float(2.0 / row_sums.max())
+    w = shapes.weights
+    # per-row sums are independent (each row is its own numpy reduction), so
+    # row chunks on the pool give numpy's bits; the max is order-free
+    rows_per = max(1, _par.PAR_MIN // max(1, w.shape[1]))
+    if w.shape[0] <= rows_per:
+        return float(2.0 / np.abs(w).sum(axis=1).max())
+    peaks = _par.chunked(w.shape[0], lambda lo, hi: np.abs(w[lo:hi]).sum(axis=1).max(), chunk=rows_per)
+    return float(2.0 / max(peaks))
 
 
 def effective_threads(requested: int) -> int:

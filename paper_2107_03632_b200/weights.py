@@ -132,7 +132,9 @@ def assemble_shapes(nodes, stencils, degree: int, workers: int = 1, device: int 
         raise ParameterError(f"support size {n} below the {monomial_count(degree)} monomials "
                              f"of degree {degree}")
     interior = nodes.interior_indices.astype(np.int64)
-    rows = stencils.neighbors[interior]
+    from .solver import _interior_rows
+
+    rows = _interior_rows(stencils.neighbors, interior)  # a view when interior = [B, N): no 8n B/row copy
     weights, status = _assemble(nodes.positions, rows, degree, device)
     if status is not None:
         hit = _resolve_flagged(status, lambda k: nodes.positions[rows[k]], degree)

@@ -156,3 +156,36 @@ def test_parallel_host_reductions_have_numpy_bits():
         assert _par.pairwise_sum(x) == float(np.add.reduce(x))
         idx = rng.integers(0, n, n // 2 + 1)
         assert np.array_equal(_par.scaled_gather(2.0 * np.pi**2, x, idx), 2.0 * np.pi**2 * x[idx])
+
+
+def test_parallel_stability_bound_has_numpys_bits():
+    """solver.stability_bound splits rows over the pool: same bits as
+    2 / np.abs(w).sum(axis=1).max() (solver.py:249-254)."""
+    from paper_2107_03632_b200.problem import ShapeStore, StencilSet
+    from paper_2107_03632_b200.solver import stability_bound
+
+    rng = np.random.default_rng(5)
+    for rows, n in ((10, 15), (100_000, 15), (70_001, 56)):
+        w = rng.normal(size=(rows, n)) * rng.uniform(0.1, 10.0, size=(rows, 1))
+        shapes = ShapeStore(degree=2, interior_nodes=np.arange(rows), weights=w,
+                            stencils=StencilSet(n=n, neighbors=np.zeros((rows, n), dtype=np.int64)))
+        assert stability_bound(shapes) == float(2.0 / np.abs(w).sum(axis=1).max())
+
+
+def test_closed_form_and_gather_into_out_have_the_same_bits():
+    """run_time_loop evaluates into page-locked scratch arrays (out=): same
+    values as the allocating calls."""
+    from paper_2107_03632_b200 import _par
+    from paper_2107_03632_b200.problem import closed_form_solution
+
+    rng = np.random.default_rng(3)
+    for n in (10, 300_000):
+        pts = rng.uniform(-1, 1, size=(n, 2))
+        want = np.sin(np.pi * pts[:, 0]) * np.sin(np.pi * pts[:, 1])
+        out = np.full(n, np.nan)
+        assert closed_form_solution(pts, out=out) is out
+        assert np.array_equal(out, want)
+        idx = rng.integers(0, n, size=n // 2)
+        g = np.full(idx.size, np.nan)
+        _par.scaled_gather(2.0 * np.pi**2, want, idx, out=g)
+        assert np.array_equal(g, 2.0 * np.pi**2 * want[idx])
