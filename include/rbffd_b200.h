@@ -128,6 +128,12 @@ int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows
  */
 int rbf_knn(const double* positions, int64_t N, int32_t n, int64_t* neighbors_out, int32_t device);
 
+/* rbf_knn for a subset of query nodes (a rank's own rows in a partitioned
+ * setup): row q of neighbors_out[n_query*n] lists the n nearest of ALL N
+ * nodes to node query_ids[q], same order and tie rule. */
+int rbf_knn_subset(const double* positions, int64_t N, int32_t n, const int64_t* query_ids, int64_t n_query,
+                   int64_t* neighbors_out, int32_t device);
+
 /*
  * The reference's advancing-front node set on the unit disk (SURVEY.md §8f
  * row 4; rbffd.geometry.generate_unit_disk_nodes, geometry.py:105-198),
@@ -155,7 +161,9 @@ int rbf_plan_create_assembled(rbf_plan** out, int64_t N, int64_t N_i, int32_t n,
                               uint32_t flags, uint8_t* row_status);
 
 /* max_k sum_j |w_kj| of the plan's weights (stability_bound = 2 / this,
- * solver.py:249-254), for plans whose weights never left the device. */
+ * solver.py:249-254), for plans whose weights never left the device.  Each
+ * row is summed in numpy's pairwise order (np.abs(w).sum(axis=1)), so the
+ * result has the reference's bits. */
 int rbf_plan_weight_row_sum_max(rbf_plan* plan, double* out);
 
 /*
@@ -314,6 +322,15 @@ int rbf_group_push_local(rbf_group* group);
 int rbf_group_push_export(rbf_group* group, void* blob_out, int64_t capacity, int64_t* length);
 int rbf_group_push_import(rbf_group* group, int32_t n_blobs, const void* blobs, int64_t stride);
 int rbf_group_push_mode(const rbf_group* group);
+
+/* Host-paced push mode: after every fixed-mode step (and its halo pushes)
+ * the group synchronises its stream and calls fn(ctx) -- a barrier across
+ * the ranks -- so no step kernel waits on a kernel of another process.  For
+ * ranks that share one GPU (time-sliced contexts give no co-scheduling
+ * guarantee), e.g. the cross-process test of the IPC push path; NULL turns
+ * it off.  Fixed-step runs of groups without NCCL return each rank's own
+ * residual / first bad step; the caller reduces them across ranks. */
+int rbf_group_set_step_barrier(rbf_group* g, void (*fn)(void*), void* ctx);
 int rbf_group_push_off(rbf_group* group);  /* back to pack + NCCL / copy (all ranks must agree) */
 
 void rbf_plan_destroy(rbf_plan* plan);

@@ -69,6 +69,8 @@ EXPORTED = (
     "rbf_error_norms",
     "rbf_host_alloc",
     "rbf_host_free_pinned",
+    "rbf_group_set_step_barrier",
+    "rbf_knn_subset",
 )
 
 
@@ -168,6 +170,8 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "rbf_error_norms": ([vp, vp, pdbl, pdbl], i32),
         "rbf_host_alloc": ([i64, ctypes.POINTER(vp)], i32),
         "rbf_host_free_pinned": ([vp], None),
+        "rbf_group_set_step_barrier": ([vp, vp, vp], i32),
+        "rbf_knn_subset": ([vp, i64, i32, vp, i64, vp, i32], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -62,7 +62,19 @@ struct StepArgs {
   // part's buffers (wait_flags[id] counts neighbour id's pushes), or null
   const unsigned long long* wait_flags;
   unsigned long long wait_mask;  // bit i: part i is a neighbour
+  unsigned long long wait_ns;    // a wait longer than this traps (a peer died)
+  long long halo_row0;           // rows >= this read halo values; the TMA step waits
+                                 // for the peers only before those (interior rows first)
+  unsigned long long* trace;     // RBFFD_TRACE diagnostics: per (step, CTA) globaltimer
+                                 // {entry, dependency resolved, ring issued, exit}, or null
+  int trace_cap;                 // steps the trace buffer holds
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 constexpr int kMaxPushPeers = 8;
 
@@ -78,10 +90,11 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
 // writes into its peers).  One lane of the CTA's first consumer warp polls
 // with acquire loads; the other consumer warps are released by a named
 // barrier (nthreads = all consumer threads), which orders their field reads
-// after the acquire.  A wait longer than ~20 s means a peer died: trap
-// instead of hanging the GPU.
+// after the acquire.  A wait longer than wait_ns (20 s; RBFFD_WAIT_TIMEOUT_MS)
+// means a peer died: trap instead of hanging the GPU.
 __device__ __forceinline__ void wait_peers(const unsigned long long* flags, unsigned long long mask,
-                                           DevStatus* st, bool first_warp, int nthreads) {
+                                           DevStatus* st, bool first_warp, int nthreads,
+                                           unsigned long long wait_ns = 20000000000ull) {
   if (!flags) return;
   if (first_warp && (threadIdx.x & 31) == 0) {
     const unsigned long long need = static_cast<unsigned long long>(
@@ -95,11 +108,34 @@ __device__ __forceinline__ void wait_peers(const unsigned long long* flags, unsi
         __nanosleep(64);
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > 20000000000ull) __trap();
+        if (t - t0 > wait_ns) __trap();
       }
     }
   }
   asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+}
+
+// Per-warp variant of wait_peers for the TMA step: lane 0 polls, the warp
+// barrier orders the other lanes' field reads after its acquire loads.
+__device__ __forceinline__ void wait_peers_warp(const unsigned long long* flags, unsigned long long mask,
+                                                DevStatus* st, unsigned long long wait_ns) {
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned long long need = static_cast<unsigned long long>(
+        *reinterpret_cast<volatile long long*>(&st->push_base) +
+        *reinterpret_cast<volatile long long*>(&st->push_count));
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (unsigned long long m = mask; m; m &= m - 1) {
+      const int j = __ffsll(static_cast<long long>(m)) - 1;
+      while (ld_acquire_sys_u64(flags + j) < need) {
+        __nanosleep(64);
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > wait_ns) __trap();
+      }
+    }
+  }
+  __syncwarp();
 }
 
 enum StepFlags : int {
@@ -263,7 +299,7 @@ step_stream_kernel(StepArgs a, const double* u_in, double* u_out, int flags) {
   const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
   // loop already stopped (push-mode groups keep stepping: the peers wait on us)
   if (!a.wait_flags && ((bs >= 0 && bs < gstep) || (cs >= 0 && cs < gstep))) return;
-  wait_peers(a.wait_flags, a.wait_mask, a.st, threadIdx.x < 32, static_cast<int>(blockDim.x));
+  wait_peers(a.wait_flags, a.wait_mask, a.st, threadIdx.x < 32, static_cast<int>(blockDim.x), a.wait_ns);
   const double dt = st->dt;
 
   bool bad = false;

@@ -80,6 +80,7 @@ struct rbf_group {
   rbf::DevStatus** d_status = nullptr;  // device array of the parts' status pointers
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaGraphExec_t fast_graph = nullptr;  // kGroupGraph fixed-mode steps (pack, exchange, step)
+  std::vector<int64_t> graph_launches;   // per part: kernel launches inside fast_graph
   long long* d_red = nullptr;            // [2] end-of-run reduction: {first bad step key, residual bits}
   // push mode (fixed-step fast path): halos stored straight into the peers'
   // buffers by push_halo_kernel, arrivals signalled through per-part counters
@@ -87,6 +88,12 @@ struct rbf_group {
   std::vector<rbf::PushArgs> push_args;  // per local part
   std::vector<unsigned int*> tickets;
   std::vector<void*> ipc_opened;         // IPC mappings to close on destroy
+  // host-paced push mode (rbf_group_set_step_barrier): every fixed-mode step
+  // is followed by a stream sync and this callback (a barrier across the
+  // ranks), so no step kernel ever waits on a kernel of another process that
+  // may not be running -- the cross-process path on ranks sharing one GPU
+  void (*step_barrier)(void*) = nullptr;
+  void* step_barrier_ctx = nullptr;
 };
 
 // What one part publishes so that its peers can push into it (IPC mode).
@@ -271,11 +278,19 @@ int group_fast_graph(rbf_group* g, cudaGraphExec_t* out) {
     *out = g->fast_graph;
     return RBF_OK;
   }
+  std::vector<int64_t> before;
+  for (rbf_plan* p : g->parts) before.push_back(p->launches);
   RBF_CK(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
   int rc = RBF_OK;
   for (int i = 0; i < kGroupGraph && rc == RBF_OK; ++i) rc = group_fast_step(g, i & 1, 0);
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(g->stream, &graph);
+  // captured launches are counted when the graph runs
+  g->graph_launches.assign(g->parts.size(), 0);
+  for (size_t a = 0; a < g->parts.size(); ++a) {
+    g->graph_launches[a] = g->parts[a]->launches - before[a];
+    g->parts[a]->launches = before[a];
+  }
   if (rc != RBF_OK) {
     if (graph) cudaGraphDestroy(graph);
     return rc;
@@ -297,15 +312,27 @@ int group_run_fast(rbf_group* g, int64_t limit, bool* any_bad, unsigned long lon
     RBF_CK(cudaMemcpyAsync(p->u_init, p->U[0], sizeof(double) * p->N, cudaMemcpyDeviceToDevice, g->stream));
   }
   cudaGraphExec_t graph = nullptr;
-  if (limit > kGroupGraph) RBF_TRY(group_fast_graph(g, &graph));
+  const bool paced = g->step_barrier != nullptr;
+  if (limit > kGroupGraph && !paced) RBF_TRY(group_fast_graph(g, &graph));
+  if (paced) {  // every rank finished its setup / previous run
+    RBF_CK(cudaStreamSynchronize(g->stream));
+    g->step_barrier(g->step_barrier_ctx);
+  }
   RBF_CK(cudaEventRecord(g->ev0, g->stream));
-  const int64_t chunks = (limit - 1) / kGroupGraph;
-  for (int64_t c = 0; c < chunks; ++c) RBF_CK(cudaGraphLaunch(graph, g->stream));
-  for (int64_t s = chunks * kGroupGraph; s < limit; ++s)
+  const int64_t chunks = paced ? 0 : (limit - 1) / kGroupGraph;
+  for (int64_t c = 0; c < chunks; ++c) {
+    RBF_CK(cudaGraphLaunch(graph, g->stream));
+    for (size_t a = 0; a < g->parts.size(); ++a) g->parts[a]->launches += g->graph_launches[a];
+  }
+  for (int64_t s = chunks * kGroupGraph; s < limit; ++s) {
     RBF_TRY(group_fast_step(g, static_cast<int>(s & 1), s == limit - 1 ? rbf::kNeedResidual : 0));
+    if (paced) {  // this step and its pushes are complete on every rank before any rank steps on
+      RBF_CK(cudaStreamSynchronize(g->stream));
+      g->step_barrier(g->step_barrier_ctx);
+    }
+  }
   RBF_CK(cudaEventRecord(g->ev1, g->stream));
   for (rbf_plan* p : g->parts) {
-    p->launches += 2 * limit;
     if (g->push) p->push_base += limit;  // every part ran all `limit` pushes
   }
   // end-of-run reduction over all parts: min first-bad-step, max residual bits
@@ -388,6 +415,28 @@ int rbf_plan_set_halo(rbf_plan* p, int32_t n_peers, const int32_t* peers, const 
   if (total > 0)
     RBF_CK(cudaMemcpyAsync(p->halo_send_idx, idx.data(), sizeof(int32_t) * total, cudaMemcpyHostToDevice,
                            p->stream));
+  // first row that reads a halo value: the TMA step overlaps the rows before
+  // it with the neighbours' pushes (parts order their rows interior-first)
+  int64_t h_lo = p->B, h_hi = 0;
+  for (int i = 0; i < n_peers; ++i)
+    if (recv_counts[i] > 0) {
+      h_lo = std::min<int64_t>(h_lo, recv_offsets[i]);
+      h_hi = std::max<int64_t>(h_hi, recv_offsets[i] + recv_counts[i]);
+    }
+  p->halo_row0 = p->N_i;
+  if (h_hi > h_lo && p->N_i > 0) {
+    unsigned long long* d_first = nullptr;
+    RBF_TRY(pool_alloc(&d_first, 1, p->stream));
+    RBF_CK(cudaMemsetAsync(d_first, 0xff, sizeof(unsigned long long), p->stream));
+    const int blocks = static_cast<int>(std::min<int64_t>((p->S * 32 * p->n + 255) / 256, 148 * 16));
+    rbf::first_row_reading_kernel<<<blocks, 256, 0, p->stream>>>(p->C, p->N_i, p->n, h_lo, h_hi, d_first);
+    RBF_CK(cudaGetLastError());
+    unsigned long long first = 0;
+    RBF_CK(cudaMemcpyAsync(&first, d_first, sizeof(first), cudaMemcpyDeviceToHost, p->stream));
+    RBF_CK(cudaStreamSynchronize(p->stream));
+    pool_free(d_first, p->stream);
+    if (first != ~0ull) p->halo_row0 = static_cast<int64_t>(first);
+  }
   RBF_CK(cudaStreamSynchronize(p->stream));
   return RBF_OK;
 }
@@ -658,6 +707,13 @@ int rbf_group_push_import(rbf_group* g, int32_t n_blobs, const void* blobs, int6
 }
 
 int rbf_group_push_mode(const rbf_group* g) { return g && g->push ? 1 : 0; }
+
+int rbf_group_set_step_barrier(rbf_group* g, void (*fn)(void*), void* ctx) {
+  if (!g) return fail(RBF_ERR_PARAM, "group is NULL");
+  g->step_barrier = fn;
+  g->step_barrier_ctx = ctx;
+  return RBF_OK;
+}
 
 // Back to the pack + NCCL / copy exchange (every rank must agree: used when
 // some rank could not map its neighbours).

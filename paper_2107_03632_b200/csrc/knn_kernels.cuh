@@ -59,10 +59,11 @@ __global__ void __launch_bounds__(128) knn_query_kernel(const double* __restrict
                                                          KnnGrid g, const unsigned int* __restrict__ start,
                                                          const int* __restrict__ sorted, int k,
                                                          long long q0, long long nq,
-                                                         long long* __restrict__ out) {
+                                                         long long* __restrict__ out,
+                                                         const long long* __restrict__ qids = nullptr) {
   for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < nq;
        t += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long qi = q0 + t;
+    const long long qi = qids ? qids[q0 + t] : q0 + t;  // query node (all nodes, or a subset)
     const double qx = pos[2 * qi], qy = pos[2 * qi + 1];
     const int cx = knn_cell_x(g, qx), cy = knn_cell_y(g, qy);
     double bd[KMAX];

@@ -23,6 +23,8 @@
 #include <cub/cub.cuh>
 
 #include <cuda_runtime.h>
+#include <emmintrin.h>
+#include <omp.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -251,6 +253,9 @@ struct rbf_plan {
   int* halo_send_idx = nullptr;     // [halo_send_total] local ids of owned nodes to send
   double* halo_sendbuf = nullptr;   // packed values, segments per peer
   int64_t halo_send_total = 0;
+  int64_t halo_row0 = 0;            // first row that reads a halo node (rbf_plan_set_halo)
+  unsigned long long* trace = nullptr;  // RBFFD_TRACE=<file>: per-step CTA timestamps of the TMA step
+  int trace_cap = 0;
 
   rbf::StepArgs args() const {
     rbf::StepArgs a;
@@ -266,6 +271,15 @@ struct rbf_plan {
     a.wait_flags = push ? push_flags : nullptr;
     a.wait_mask = 0;
     for (int i = 0; push && i < wait_n; ++i) a.wait_mask |= 1ull << wait_ids[i];
+    static const unsigned long long wait_ns = [] {
+      const char* e = std::getenv("RBFFD_WAIT_TIMEOUT_MS");
+      const long long ms = e ? std::atoll(e) : 20000;
+      return static_cast<unsigned long long>(ms > 0 ? ms : 20000) * 1000000ull;
+    }();
+    a.wait_ns = wait_ns;
+    a.halo_row0 = push ? halo_row0 : 0;
+    a.trace = trace;
+    a.trace_cap = trace_cap;
     return a;
   }
 };
@@ -343,6 +357,27 @@ void status_free(rbf::DevStatus* p) {
   StatusSlab& sl = status_slab();
   std::lock_guard<std::mutex> lock(sl.mu);
   sl.free_list.push_back(p);
+}
+
+// Staging copies with non-temporal (streaming) stores: the pinned staging
+// buffer is written once and read only by the DMA engine.
+void copy_f64_nt(double* dst, const double* src, int64_t count) {
+  int64_t i = 0;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) && count > 0) {
+    dst[0] = src[0];
+    i = 1;
+  }
+  for (; i + 2 <= count; i += 2) _mm_stream_pd(dst + i, _mm_loadu_pd(src + i));
+  for (; i < count; ++i) dst[i] = src[i];
+}
+int narrow_ids_nt(int32_t* dst, const int64_t* src, int64_t count, int64_t N) {
+  int bad = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t v = src[i];
+    bad |= (v < 0 || v >= N);
+    _mm_stream_si32(dst + i, static_cast<int32_t>(v));
+  }
+  return bad;
 }
 
 // Pinned, double-buffered staging for plan uploads: the host copies (and
@@ -1108,6 +1143,11 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
       cudaGetLastError();
     }
   }
+  if (p->tma_fn && std::getenv("RBFFD_TRACE")) {  // diagnostics: CTA timelines of up to 4096 steps
+    p->trace_cap = 4096;
+    RBF_TRY(dev_alloc(p.get(), &p->trace, static_cast<size_t>(p->trace_cap) * p->grid * 4));
+    RBF_CK(cudaMemsetAsync(p->trace, 0, sizeof(unsigned long long) * p->trace_cap * p->grid * 4, p->stream));
+  }
   if (!p->tma_fn) {
     RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p->stream_fn, kStreamBlock, 0));
     per_sm = std::max(per_sm, 1);
@@ -1306,11 +1346,17 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
       double* hw = hf + cnt;
       int bad = 0;
       const int64_t* src_c = rows + k0 * n;
-#pragma omp parallel for schedule(static) reduction(| : bad)
-      for (int64_t e = 0; e < total; ++e) {
-        const int64_t v = src_c[e];
-        bad |= (v < 0 || v >= N);
-        hc[e] = static_cast<int32_t>(v);
+      const double* src_w = assemble ? nullptr : weights + k0 * n;
+      // one pass per thread over a contiguous range: ids range-checked and
+      // narrowed, weights copied, both with non-temporal stores (the staging
+      // buffer is only read again by the DMA: no read-for-ownership traffic)
+#pragma omp parallel reduction(| : bad)
+      {
+        const int64_t T = omp_get_num_threads(), t = omp_get_thread_num();
+        const int64_t lo = total * t / T, hi = total * (t + 1) / T;
+        bad |= narrow_ids_nt(hc + lo, src_c + lo, hi - lo, N);
+        if (src_w) copy_f64_nt(hw + lo, src_w + lo, hi - lo);
+        _mm_sfence();
       }
       if (bad) {
         ids_ok = false;
@@ -1318,11 +1364,6 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
       }
       if (f_int) std::memcpy(hf, f_int + k0, sizeof(double) * cnt);
       else std::memset(hf, 0, sizeof(double) * cnt);  // forcing set later (rbf_set_forcing)
-      if (!assemble) {
-        const double* src_w = weights + k0 * n;
-#pragma omp parallel for schedule(static)
-        for (int64_t e = 0; e < total; ++e) hw[e] = src_w[e];
-      }
       RBF_CK(cudaMemcpyAsync(d_c, hc, sizeof(int32_t) * total, cudaMemcpyHostToDevice, p->stream));
       RBF_CK(cudaMemcpyAsync(d_f, hf, sizeof(double) * cnt, cudaMemcpyHostToDevice, p->stream));
       if (assemble) {  // weights computed on the device, never on the host
@@ -1492,7 +1533,16 @@ int rbf_assemble_weights(const double* positions, int64_t N, const int64_t* rows
 }
 
 int rbf_knn(const double* positions, int64_t N, int32_t n, int64_t* neighbors_out, int32_t device) {
+  return rbf_knn_subset(positions, N, n, nullptr, N, neighbors_out, device);
+}
+
+int rbf_knn_subset(const double* positions, int64_t N, int32_t n, const int64_t* query_ids, int64_t n_query,
+                   int64_t* neighbors_out, int32_t device) {
   if (!positions || !neighbors_out) return fail(RBF_ERR_PARAM, "NULL argument");
+  if (n_query < 0 || (!query_ids && n_query != N)) return fail(RBF_ERR_PARAM, "bad query set");
+  if (query_ids)
+    for (int64_t q = 0; q < n_query; ++q)
+      if (query_ids[q] < 0 || query_ids[q] >= N) return fail(RBF_ERR_PARAM, "query node id out of range");
   if (N < 1 || N > std::numeric_limits<int32_t>::max()) return fail(RBF_ERR_PARAM, "N must be in [1, 2^31-1]");
   if (n < 1 || n > N) return fail(RBF_ERR_PARAM, "support size n=" + std::to_string(n) + " outside [1, N]");
   if (n > 128) return fail(RBF_ERR_PARAM, "support size above 128 is not supported on the GPU path");
@@ -1527,9 +1577,10 @@ int rbf_knn(const double* positions, int64_t N, int32_t n, int64_t* neighbors_ou
   unsigned int* d_count = nullptr;
   unsigned int* d_start = nullptr;
   long long* d_out = nullptr;
+  long long* d_q = nullptr;
   void* d_tmp = nullptr;
   size_t tmp_bytes = 0;
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(N, (int64_t(1) << 25) / n));
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(n_query, 1), (int64_t(1) << 25) / n));
   int rc = RBF_OK;
   auto ck = [&](cudaError_t e, const char* what) {
     if (rc == RBF_OK && e != cudaSuccess) rc = fail(RBF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -1541,6 +1592,10 @@ int rbf_knn(const double* positions, int64_t N, int32_t n, int64_t* neighbors_ou
   ck(cudaMallocAsync(&d_start, sizeof(unsigned int) * (cells + 1), st), "alloc");
   ck(cudaMallocAsync(&d_out, sizeof(long long) * chunk * n, st), "alloc");
   ck(cudaMemcpyAsync(d_pos, positions, sizeof(double) * 2 * N, cudaMemcpyHostToDevice, st), "upload");
+  if (query_ids && n_query > 0) {
+    ck(cudaMallocAsync(&d_q, sizeof(long long) * n_query, st), "alloc");
+    ck(cudaMemcpyAsync(d_q, query_ids, sizeof(long long) * n_query, cudaMemcpyHostToDevice, st), "upload");
+  }
   ck(cudaMemsetAsync(d_count, 0, sizeof(unsigned int) * (cells + 1), st), "memset");
   const int blocks = static_cast<int>(std::min<int64_t>((N + 255) / 256, 148 * 16));
   if (rc == RBF_OK) {
@@ -1553,13 +1608,13 @@ int rbf_knn(const double* positions, int64_t N, int32_t n, int64_t* neighbors_ou
     rbf::knn_fill_kernel<<<blocks, 256, 0, st>>>(d_cell, N, d_count, d_sorted);
     ck(cudaGetLastError(), "fill");
   }
-  for (int64_t q0 = 0; q0 < N && rc == RBF_OK; q0 += chunk) {
-    const int64_t nq = std::min<int64_t>(chunk, N - q0);
+  for (int64_t q0 = 0; q0 < n_query && rc == RBF_OK; q0 += chunk) {
+    const int64_t nq = std::min<int64_t>(chunk, n_query - q0);
     const int qb = static_cast<int>(std::min<int64_t>((nq + 127) / 128, 148 * 32));
-    if (n <= 16) rbf::knn_query_kernel<16><<<qb, 128, 0, st>>>(d_pos, N, g, d_start, d_sorted, n, q0, nq, d_out);
-    else if (n <= 32) rbf::knn_query_kernel<32><<<qb, 128, 0, st>>>(d_pos, N, g, d_start, d_sorted, n, q0, nq, d_out);
-    else if (n <= 64) rbf::knn_query_kernel<64><<<qb, 128, 0, st>>>(d_pos, N, g, d_start, d_sorted, n, q0, nq, d_out);
-    else rbf::knn_query_kernel<128><<<qb, 128, 0, st>>>(d_pos, N, g, d_start, d_sorted, n, q0, nq, d_out);
+    if (n <= 16) rbf::knn_query_kernel<16><<<qb, 128, 0, st>>>(d_pos, N, g, d_start, d_sorted, n, q0, nq, d_out, d_q);
+    else if (n <= 32) rbf::knn_query_kernel<32><<<qb, 128, 0, st>>>(d_pos, N, g, d_start, d_sorted, n, q0, nq, d_out, d_q);
+    else if (n <= 64) rbf::knn_query_kernel<64><<<qb, 128, 0, st>>>(d_pos, N, g, d_start, d_sorted, n, q0, nq, d_out, d_q);
+    else rbf::knn_query_kernel<128><<<qb, 128, 0, st>>>(d_pos, N, g, d_start, d_sorted, n, q0, nq, d_out, d_q);
     ck(cudaGetLastError(), "query");
     ck(cudaMemcpyAsync(neighbors_out + q0 * n, d_out, sizeof(long long) * nq * n, cudaMemcpyDeviceToHost, st),
        "download");
@@ -1571,6 +1626,7 @@ int rbf_knn(const double* positions, int64_t N, int32_t n, int64_t* neighbors_ou
   cudaFreeAsync(d_count, st);
   cudaFreeAsync(d_start, st);
   cudaFreeAsync(d_out, st);
+  if (d_q) cudaFreeAsync(d_q, st);
   if (d_tmp) cudaFreeAsync(d_tmp, st);
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
@@ -1979,6 +2035,17 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
   float ms = 0.f;
   RBF_CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
   const rbf::DevStatus s = *p->h_st;
+  if (p->trace && limit > 0) {  // RBFFD_TRACE: append {grid, steps, [steps][grid][4] ns} to the file
+    const int64_t n_tr = std::min<int64_t>(limit, p->trace_cap);
+    std::vector<unsigned long long> h(static_cast<size_t>(n_tr) * p->grid * 4);
+    RBF_CK(cudaMemcpy(h.data(), p->trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    if (std::FILE* f = std::fopen(std::getenv("RBFFD_TRACE"), "ab")) {
+      const int64_t hdr[2] = {p->grid, n_tr};
+      std::fwrite(hdr, sizeof(hdr), 1, f);
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      std::fclose(f);
+    }
+  }
 
   int64_t done = limit > 0 && p->N_i > 0 ? s.step : limit;
   bool have_res = false;
@@ -2123,6 +2190,7 @@ void rbf_plan_destroy(rbf_plan* p) {
     pool_free(p->U[1], s);
   }
   pool_free(p->tmp, s);
+  pool_free(p->trace, s);
   pool_free(p->d_norm_start, s);
   pool_free(p->d_norm_sum, s);
   pool_free(p->norm_exact, s);

@@ -74,9 +74,9 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
   const int stage_bytes = sps * tma_slice_bytes<NJ, IB>();
   const long long S = (a.n_rows + 31) >> 5;
   const long long nchunks = (S + sps - 1) / sps;
-  // CTA b streams chunks b, b + G, b + 2G, ... (G = gridDim.x).  Ring
-  // positions and mbarrier phases are tracked with 32-bit counters advanced
-  // incrementally: no 64-bit division on the per-unit path.
+  // CTA b streams chunks b, b + G, b + 2G, ... (G = gridDim.x).  Chunk,
+  // ring-stage and phase indices are 32-bit (no 64-bit division on the
+  // per-unit path: the SASS of a 64-bit div/mod is a subroutine call).
   const int my_n = blockIdx.x < nchunks ? static_cast<int>((nchunks - 1 - blockIdx.x) / gridDim.x + 1) : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -95,6 +95,8 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
   bool bad = false;
   unsigned long long dmax = 0ull;
   long long gstep = 0;
+  unsigned long long tr[4] = {0, 0, 0, 0};  // RBFFD_TRACE (thread 0)
+  if (a.trace && threadIdx.x == 0) tr[0] = globaltimer();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -122,6 +124,7 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
       const int pre = my_n < stages ? my_n : stages;
       for (int i = 0; i < pre; ++i) issue(i, i);  // before the dependency wait
       pdl_wait();
+      if (a.trace) tr[1] = globaltimer();
       const long long g0 = *reinterpret_cast<volatile long long*>(&st->step);
       const long long bs = *reinterpret_cast<volatile long long*>(&st->bad_step);
       const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
@@ -141,6 +144,7 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
           ph ^= 1u;
         }
       }
+      if (a.trace) tr[2] = globaltimer();
     } else {
       pdl_wait();
       const long long g0 = *reinterpret_cast<volatile long long*>(&st->step);
@@ -155,14 +159,19 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
     const long long bs = *reinterpret_cast<volatile long long*>(&st->bad_step);
     const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
     if (!a.wait_flags && ((bs >= 0 && bs < gstep) || (cs >= 0 && cs < gstep))) return;
-    wait_peers(a.wait_flags, a.wait_mask, a.st, warp == 1, 32 * CW);
+    // push-mode parts order their rows interior-first: a warp waits for the
+    // neighbours' halo pushes only before its first unit with a row >=
+    // halo_row0, so rows that read no halo value overlap the exchange
+    bool waited = a.wait_flags == nullptr;
     const double dt = st->dt;
     const int upc = sps / RPL;  // consumer units per chunk
-    // this warp's units: warp-1, warp-1+CW, ... over (chunk i, unit u)
-    int i = (warp - 1) / upc, u = (warp - 1) - i * upc;
-    int s = i % stages;
-    uint32_t ph = static_cast<uint32_t>((i / stages) & 1);
-    while (i < my_n) {
+    // this warp's units q = warp-1, warp-1+CW, ... -> (chunk i, unit u),
+    // ring stage s, phase ph (32-bit arithmetic)
+    const int total = my_n * upc;
+    for (int q = warp - 1; q < total; q += CW) {
+      const int i = q / upc, u = q - i * upc;
+      const int s = i % stages;
+      const uint32_t ph = static_cast<uint32_t>((i / stages) & 1);
       const int slot0 = u * RPL;
       if (lane == 0) {
         while (*reinterpret_cast<volatile int*>(&s_issued) <= i) __nanosleep(64);
@@ -171,6 +180,10 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
       mbar_wait(&full[s], ph);
       const unsigned char* base = ring + static_cast<size_t>(s) * stage_bytes;
       const long long slice0 = (blockIdx.x + static_cast<long long>(i) * gridDim.x) * sps + slot0;
+      if (!waited && (slice0 + RPL) * 32 > a.halo_row0) {
+        wait_peers_warp(a.wait_flags, a.wait_mask, a.st, a.wait_ns);
+        waited = true;
+      }
       {
         bool live[RPL];
         double g[RPL][NJ];
@@ -233,16 +246,17 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
       // release semantics; __syncwarp orders the other lanes' shared reads)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      u += CW;
-      while (u >= upc) {
-        u -= upc;
-        ++i;
-        if (++s == stages) {
-          s = 0;
-          ph ^= 1u;
-        }
-      }
     }
+    // every warp has waited before the step completes: the push that follows
+    // this step must not overwrite a neighbour's buffer it still reads
+    // (send-only neighbours, parts without halo rows)
+    if (!waited) wait_peers_warp(a.wait_flags, a.wait_mask, a.st, a.wait_ns);
+  }
+  if (a.trace && threadIdx.x == 0) {
+    tr[3] = globaltimer();
+    unsigned long long* o = a.trace + (static_cast<long long>(gstep % a.trace_cap) * gridDim.x + blockIdx.x) * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = tr[k];
   }
   step_epilogue(st, gstep, bad, dmax, flags);
 }
@@ -1016,15 +1030,43 @@ __global__ void decide_kernel(DevStatus* st, long long step, int flags) {
 }
 
 // max_r sum_j |w_rj| over the SELL rows (stability_bound, solver.py:249-254;
-// serial j sum per row, then an exact max over non-negative bit patterns)
+// each row summed in numpy's order (below), then an exact max over
+// non-negative bit patterns): 2 / this has the reference's auto-dt bits.
+// sum_j |w[j*32]| for j in [j0, j0+len) in numpy's pairwise order
+// (np.abs(weights).sum(axis=1) reduces each row on its own: pairwise_sum of
+// loops_utils.h.src, 8 accumulators up to 128 entries, halving above)
+__device__ double pairwise_abs_row(const double* __restrict__ w, int j0, int len) {
+  if (len < 8) {
+    double res = 0.0;
+    for (int i = 0; i < len; ++i) res = __dadd_rn(res, fabs(w[32LL * (j0 + i)]));
+    return res;
+  }
+  if (len <= 128) {
+    double r[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r[q] = fabs(w[32LL * (j0 + q)]);
+    int i = 8;
+    for (; i < len - (len % 8); i += 8) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], fabs(w[32LL * (j0 + i + q)]));
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < len; ++i) res = __dadd_rn(res, fabs(w[32LL * (j0 + i)]));
+    return res;
+  }
+  int n2 = len / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_abs_row(w, j0, n2), pairwise_abs_row(w, j0 + n2, len - n2));
+}
+
 __global__ void row_abs_sum_max_kernel(const double* __restrict__ W, long long n_rows, int n,
                                        double* out) {
   unsigned long long m = 0ull;
   for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < n_rows;
        r += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long base = (r >> 5) * static_cast<long long>(n) * 32 + (r & 31);
-    double s = 0.0;
-    for (int j = 0; j < n; ++j) s += fabs(W[base + 32LL * j]);
+    const double s = pairwise_abs_row(W + base, 0, n);
     const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(s));
     m = b > m ? b : m;
   }
@@ -1087,6 +1129,21 @@ __global__ void scatter_rows_kernel(const double* __restrict__ f, const long lon
        k += static_cast<long long>(gridDim.x) * blockDim.x)
     F[row_of_k[k]] = f[k];
 }
+// First row whose stencil reads a node in [lo, hi) (a part's halo slice):
+// atomicMin over the SELL entries.
+__global__ void first_row_reading_kernel(const int* __restrict__ C, long long n_rows, int n, long long lo,
+                                         long long hi, unsigned long long* first) {
+  const long long total = ((n_rows + 31) >> 5) * 32LL * n;
+  unsigned long long m = ~0ull;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = (e / (32LL * n)) * 32 + (e & 31);
+    const int c = C[e];
+    if (r < n_rows && c >= lo && c < hi && static_cast<unsigned long long>(r) < m) m = r;
+  }
+  if (m != ~0ull) atomicMin(first, m);
+}
+
 // Plan-file payload check (rbf_plan_load): every streamed node id in [0, N),
 // every 16-bit id of a fitting slice decodes to its int32 id, the renumbering
 // maps stay in range.  err bits: 1 C, 2 C16/meta, 4 new_id, 8 row_of_k.

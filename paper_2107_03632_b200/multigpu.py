@@ -18,6 +18,9 @@ Partitioning (``partition``):
   so owned row r updates local node ``B_p + H_p + r`` (the plan's canonical
   layout: no renumbering on the device) and the halo of each peer is one
   contiguous slice of u -- received in place;
+* owned rows interior-first: rows that read no halo value come before the
+  rest (each group in Morton order), so the push-mode step computes them
+  while the neighbours' halos are still arriving;
 * the per-row j-order is untouched, so a partitioned run is bitwise identical
   to one GPU and to the CPU oracle.
 
@@ -116,24 +119,36 @@ def partition(n_total: int, interior: np.ndarray, rows: np.ndarray, weights: np.
     bounds = np.linspace(0, n_rows, n_parts + 1).round().astype(np.int64)
 
     owner = np.full(n_total, -1, dtype=np.int32)  # part owning each interior node
-    slot = np.full(n_total, -1, dtype=np.int64)  # row position of a node in its owner
+    mslot = np.full(n_total, -1, dtype=np.int64)  # position of a node in its owner's Morton range
     for p in range(n_parts):
         ks = perm[bounds[p]:bounds[p + 1]]
         owner[interior[ks]] = p
+        mslot[interior[ks]] = np.arange(ks.size)
+    # each part's rows interior-first: rows that read no halo value (only own
+    # and Dirichlet nodes) before the rest, each group in Morton order, so the
+    # push-mode step overlaps them with the exchange (StepArgs::halo_row0)
+    own_ks = []
+    slot = np.full(n_total, -1, dtype=np.int64)  # final row position of a node in its owner
+    for p in range(n_parts):
+        ks = perm[bounds[p]:bounds[p + 1]]
+        of = owner[rows[ks]]
+        reads_halo = ((of >= 0) & (of != p)).any(axis=1)
+        ks = ks[np.argsort(reads_halo, kind="stable")]
+        own_ks.append(ks)
         slot[interior[ks]] = np.arange(ks.size)
 
     parts: List[Part] = []
     halo_from: List[dict] = []
     for p in range(n_parts):
-        ks = perm[bounds[p]:bounds[p + 1]]
+        ks = own_ks[p]
         own_nodes = interior[ks]
         refs = rows[ks]
         uniq = np.unique(refs)
         own_of = owner[uniq]
         bnd = uniq[own_of < 0]
         halo = uniq[(own_of >= 0) & (own_of != p)]
-        # group the halo by owner, each group in the owner's row order
-        hk = np.lexsort((slot[halo], owner[halo]))
+        # group the halo by owner, each group in the owner's Morton order
+        hk = np.lexsort((mslot[halo], owner[halo]))
         halo = halo[hk]
         l2g = np.concatenate([bnd, halo, own_nodes]).astype(np.int64)
         g2l = np.full(n_total, -1, dtype=np.int64)
@@ -267,12 +282,14 @@ class LocalGroup(_Group):
     buffers after each part's step (push mode, the default); steady runs and
     failure replays use pack / device copy / step / reduce on one stream."""
 
-    def __init__(self, parts: Sequence[Part], devices: Optional[Sequence[int]] = None, push: bool = True):
+    def __init__(self, parts: Sequence[Part], devices: Optional[Sequence[int]] = None, push: bool = True,
+                 plans=None):
         from .solver import Plan
 
         devices = list(devices) if devices is not None else [0] * len(parts)
-        plans = [Plan(pt.n_local, pt.interior, pt.rows, pt.weights, pt.f_int, device=d,
-                      resident=False) for pt, d in zip(parts, devices)]
+        if plans is None:
+            plans = [Plan(pt.n_local, pt.interior, pt.rows, pt.weights, pt.f_int, device=d,
+                          resident=False) for pt, d in zip(parts, devices)]
         super().__init__(parts, plans, None, 0, 1)
         if push and len(parts) > 1:
             self._push_local()
@@ -284,14 +301,68 @@ class NcclGroup(_Group):
     NVLink through CUDA IPC mappings of the peers' buffers; steady runs and
     failure replays exchange by NCCL send/recv."""
 
-    def __init__(self, part: Part, rank: int, nranks: int, device: int, uid: bytes, allgather=None):
+    def __init__(self, part: Part, rank: int, nranks: int, device: int, uid: bytes, allgather=None,
+                 plan=None):
+        from .solver import Plan
+
+        if plan is None:
+            plan = Plan(part.n_local, part.interior, part.rows, part.weights, part.f_int,
+                        device=device, resident=False)
+        super().__init__([part], [plan], uid, rank, nranks)
+        if allgather is not None and nranks > 1:
+            self._push_ipc(allgather)
+
+
+class HostPacedGroup(_Group):
+    """One part per process, halos pushed peer-to-peer through CUDA IPC
+    mappings (the NcclGroup fast path), each step followed by a host barrier
+    (rbf_group_set_step_barrier): no step kernel waits on a kernel of another
+    process.  This is the cross-process push path for ranks that share one
+    GPU (NCCL refuses two ranks on one device, and time-sliced contexts do
+    not guarantee that waiting kernels are co-scheduled); fixed-step runs
+    only.  `allgather(bytes) -> [bytes]` and `barrier()` are the ranks'
+    control plane (e.g. torch.distributed with gloo)."""
+
+    def __init__(self, part: Part, rank: int, nranks: int, device: int, allgather, barrier):
         from .solver import Plan
 
         plan = Plan(part.n_local, part.interior, part.rows, part.weights, part.f_int,
                     device=device, resident=False)
-        super().__init__([part], [plan], uid, rank, nranks)
-        if allgather is not None and nranks > 1:
-            self._push_ipc(allgather)
+        super().__init__([part], [plan], None, rank, nranks)
+        self._allgather = allgather
+        self._push_ipc(allgather)
+        if not self.push_mode:
+            raise RuntimeError("IPC push mode could not be set up on every rank")
+        self._barrier_fn = barrier
+        self._cb = ctypes.CFUNCTYPE(None, ctypes.c_void_p)(lambda _ctx: self._barrier_fn())
+        self.plans[0]._check(self._lib.rbf_group_set_step_barrier(
+            self._h, ctypes.cast(self._cb, ctypes.c_void_p), None))
+
+    def run(self, dt, steps=0, mode="fixed", tol=1e-9, max_steps=1_000_000):
+        if mode != "fixed" or steps < 2:
+            raise ParameterError("host-paced groups run fixed-step runs of >= 2 steps")
+        rc, done, residual, bad, sec = super().run(dt, steps=steps)
+        # each rank holds its own part's residual / first bad step: reduce
+        # (max of non-negative residuals is exact; first bad step = min)
+        import struct
+
+        blobs = self._allgather(struct.pack("<qdq", bad, -1.0 if residual is None else residual, rc))
+        vals = [struct.unpack("<qdq", b) for b in blobs]
+        bads = [v[0] for v in vals if v[0] >= 0]
+        res = max(v[1] for v in vals)
+        rc = max(v[2] for v in vals)
+        return rc, done, (None if res < 0 else res), (min(bads) if bads else -1), sec
+
+
+def assembled_plan(setup, degree: int, device: int = 0):
+    """The plan of a dsetup.RankSetup part with its weights assembled on the
+    device (never on the host); streaming loop (groups step every part)."""
+    from .solver import Plan
+
+    return Plan.assembled(setup.l2g.size, np.arange(setup.B + setup.H, setup.B + setup.H + setup.n_own,
+                                                    dtype=np.int64),
+                          setup.rows, setup.positions_local, setup.f_int, degree, device=device,
+                          resident=False)
 
 
 def nccl_unique_id() -> bytes:

@@ -34,6 +34,25 @@ def build_stencils(nodes, n: int, device: int = 0) -> StencilSet:
     return StencilSet(n=n, neighbors=out)
 
 
+def build_stencils_subset(positions: np.ndarray, n: int, query: np.ndarray, device: int = 0) -> np.ndarray:
+    """Supports of the nodes `query` only (a rank's own rows): (len(query), n)
+    int64 global ids, the n nearest of all nodes, same order and ties as
+    build_stencils (rbf_knn_subset)."""
+    pos = np.ascontiguousarray(positions, dtype=np.float64)
+    q = np.ascontiguousarray(query, dtype=np.int64)
+    total = pos.shape[0]
+    if not 1 <= n <= total:
+        raise ParameterError(f"support size n={n} outside [1, N={total}]")
+    out = np.empty((q.size, n), dtype=np.int64)
+    lib = _lib.load()
+    rc = lib.rbf_knn_subset(pos.ctypes.data, total, int(n), q.ctypes.data, q.size, out.ctypes.data, int(device))
+    if rc == _lib.RBF_ERR_PARAM:
+        raise ParameterError(_lib.last_error(lib))
+    if rc != _lib.RBF_OK:
+        raise DeviceError(_lib.last_error(lib))
+    return out
+
+
 def recommended_support_size(degree: int, dim: int = 2, safety: int = 1) -> int:
     """binomial(degree + dim, degree) x safety (neighborhoods.py:38-48)."""
     if degree < 0 or dim < 1:

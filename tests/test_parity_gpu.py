@@ -928,3 +928,19 @@ def test_device_error_norms_have_numpys_bits(N, renumber):
         assert linf == float(np.max(np.abs(d)))
         assert l2 == math.sqrt(float((d**2).mean())), (N, scale)
     plan.close()
+
+
+@pytest.mark.parametrize("n", [5, 8, 12, 15, 30, 56, 64, 130])
+def test_device_stability_bound_has_numpys_bits(n):
+    """rbf_plan_weight_row_sum_max sums each row in numpy's pairwise order:
+    2 / it == stability_bound (solver.py:249-254) bit for bit."""
+    rng = np.random.default_rng(n)
+    n_rows, N = 2000, 5000
+    interior = np.arange(N - n_rows, N, dtype=np.int64)
+    rows = rng.integers(0, N, size=(n_rows, n)).astype(np.int64)
+    w = rng.normal(size=(n_rows, n)) * np.exp(rng.normal(size=(n_rows, n)) * 4)
+    plan = Plan(N, interior, rows, w, np.zeros(n_rows))
+    shapes = rb.ShapeStore(degree=2, interior_nodes=interior, weights=w,
+                           stencils=rb.StencilSet(n=n, neighbors=np.zeros((N, n), dtype=np.int64)))
+    assert 2.0 / plan.weight_row_sum_max() == rb.stability_bound(shapes)
+    plan.close()

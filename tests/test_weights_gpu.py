@@ -108,7 +108,7 @@ def test_plan_with_device_assembled_weights_is_bitwise(golden):
     f_int = rb.forcing(nodes.positions[interior])
     u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
     a = Plan.assembled(nodes.n_total, interior, rows, nodes.positions, f_int, shapes.degree)
-    assert 2.0 / a.weight_row_sum_max() == pytest.approx(rb.stability_bound(host), rel=1e-12)
+    assert 2.0 / a.weight_row_sum_max() == rb.stability_bound(host)  # numpy's row-sum bits
     dt = rb.stability_bound(host) * 0.5
     a.set_field(u0)
     ra = a.run(dt, steps=150)

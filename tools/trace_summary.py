@@ -1,0 +1,44 @@
+"""Summarise an RBFFD_TRACE file (per step and CTA: globaltimer at kernel
+entry, dependency resolved (griddepcontrol.wait), ring fully issued, exit).
+
+    RBFFD_TRACE=/tmp/t.bin python bench.py --quick ...; python tools/trace_summary.py /tmp/t.bin
+"""
+import sys
+
+import numpy as np
+
+
+def runs(path):
+    raw = np.fromfile(path, dtype=np.uint64)
+    i = 0
+    while i < raw.size:
+        G, S = int(raw[i]), int(raw[i + 1])
+        i += 2
+        yield raw[i:i + G * S * 4].reshape(S, G, 4).astype(np.int64)
+        i += G * S * 4
+
+
+def summarise(t):
+    S = t.shape[0]
+    entry, wait, issued, exit_ = t[:, :, 0], t[:, :, 1], t[:, :, 2], t[:, :, 3]
+    span = exit_.max(1) - wait.min(1)
+    imb = exit_.max(1) - exit_.min(1)
+    gap = wait.min(1)[1:] - exit_.max(1)[:-1]  # dependency resolution after the previous step's last CTA
+    early = entry.min(1)[1:] - exit_.max(1)[:-1]  # next step's first CTA entry vs this step's end
+    prod = issued.max(1) - wait.min(1)
+    period = exit_.max(1)[1:] - exit_.max(1)[:-1]
+    us = lambda x: f"{np.median(x) / 1e3:7.2f}"
+    print(f"steps {S}  CTAs {t.shape[1]}")
+    print(f"  period (last exit to last exit)          {us(period)} us")
+    print(f"  compute span (first dep. resolved -> last exit) {us(span)} us")
+    print(f"  exit imbalance (first -> last CTA exit)  {us(imb)} us")
+    print(f"  dependency gap (last exit -> next first resolved) {us(gap)} us")
+    print(f"  next step's first CTA entry vs last exit {us(early)} us (negative: PDL prelaunch)")
+    print(f"  producer: ring issued (last CTA) after first resolved {us(prod)} us")
+
+
+if __name__ == "__main__":
+    for k, t in enumerate(runs(sys.argv[1])):
+        print(f"== run {k}")
+        if t.shape[0] > 2:
+            summarise(t[1:])  # the first step has no predecessor
