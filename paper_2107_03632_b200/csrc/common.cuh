@@ -145,6 +145,7 @@ enum StepFlags : int {
                       // all-reduce + decide_kernel finalise the step
 };
 
+
 // ---- load helpers --------------------------------------------------------
 // Streamed, read-once data (weights, ids, forcing): bypass L1, L2 evict-first,
 // so they do not push the gathered field out of L2.

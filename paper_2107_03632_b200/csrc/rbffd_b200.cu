@@ -1182,20 +1182,22 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
   // ---- validation (host, parallel: parameter errors before any CUDA call) ----
   PhaseTimer timer;
   const int64_t B = N - N_i;
+  // range check + membership marks with plain stores; the ids are distinct
+  // iff exactly N_i marks end up set (a duplicate marks one entry twice)
   std::vector<uint8_t> seen(static_cast<size_t>(N), 0);
-  int bad_range = 0, bad_dup = 0, ident = morton ? 0 : 1;
-#pragma omp parallel for schedule(static) reduction(| : bad_range, bad_dup) reduction(& : ident)
+  int bad_range = 0, ident = morton ? 0 : 1;
+#pragma omp parallel for schedule(static) reduction(| : bad_range) reduction(& : ident)
   for (int64_t k = 0; k < N_i; ++k) {
     const int64_t v = interior[k];
-    if (v < 0 || v >= N) {
-      bad_range = 1;
-    } else if (__atomic_fetch_or(&seen[v], static_cast<uint8_t>(1), __ATOMIC_RELAXED)) {
-      bad_dup = 1;
-    }
+    if (v < 0 || v >= N) bad_range = 1;
+    else seen[v] = 1;
     if (v != B + k) ident = 0;
   }
   if (bad_range) return fail(RBF_ERR_PARAM, "interior node id out of range");
-  if (bad_dup) return fail(RBF_ERR_PARAM, "interior node ids must be distinct");
+  int64_t marked = 0;
+#pragma omp parallel for schedule(static) reduction(+ : marked)
+  for (int64_t i = 0; i < N; ++i) marked += seen[i];
+  if (marked != N_i) return fail(RBF_ERR_PARAM, "interior node ids must be distinct");
   const bool identity = ident != 0;
   double xmin = 0, xmax = 0, ymin = 0, ymax = 0;
   if (morton && N_i > 1) {

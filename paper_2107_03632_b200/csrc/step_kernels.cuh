@@ -95,8 +95,10 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
   bool bad = false;
   unsigned long long dmax = 0ull;
   long long gstep = 0;
-  unsigned long long tr[4] = {0, 0, 0, 0};  // RBFFD_TRACE (thread 0)
+#ifdef RBF_TRACE
+  unsigned long long tr[4] = {0, 0, 0, 0};  // RBFFD_TRACE (thread 0; built with make TRACE=1)
   if (a.trace && threadIdx.x == 0) tr[0] = globaltimer();
+#endif
 
   if (warp == 0) {
     if (lane == 0) {
@@ -124,7 +126,9 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
       const int pre = my_n < stages ? my_n : stages;
       for (int i = 0; i < pre; ++i) issue(i, i);  // before the dependency wait
       pdl_wait();
+#ifdef RBF_TRACE
       if (a.trace) tr[1] = globaltimer();
+#endif
       const long long g0 = *reinterpret_cast<volatile long long*>(&st->step);
       const long long bs = *reinterpret_cast<volatile long long*>(&st->bad_step);
       const long long cs = *reinterpret_cast<volatile long long*>(&st->conv_step);
@@ -144,7 +148,9 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
           ph ^= 1u;
         }
       }
+#ifdef RBF_TRACE
       if (a.trace) tr[2] = globaltimer();
+#endif
     } else {
       pdl_wait();
       const long long g0 = *reinterpret_cast<volatile long long*>(&st->step);
@@ -252,13 +258,15 @@ step_tma_kernel(StepArgs a, const double* u_in, double* u_out, int flags, TmaGeo
     // (send-only neighbours, parts without halo rows)
     if (!waited) wait_peers_warp(a.wait_flags, a.wait_mask, a.st, a.wait_ns);
   }
-  if (a.trace && threadIdx.x == 0) {
+  step_epilogue(st, gstep, bad, dmax, flags);
+#ifdef RBF_TRACE
+  if (a.trace && threadIdx.x == 0) {  // after the epilogue: the CTA's consumers are done
     tr[3] = globaltimer();
     unsigned long long* o = a.trace + (static_cast<long long>(gstep % a.trace_cap) * gridDim.x + blockIdx.x) * 4;
 #pragma unroll
     for (int k = 0; k < 4; ++k) o[k] = tr[k];
   }
-  step_epilogue(st, gstep, bad, dmax, flags);
+#endif
 }
 
 // ---------------------------------------------------------------------------

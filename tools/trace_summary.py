@@ -1,5 +1,6 @@
 """Summarise an RBFFD_TRACE file (per step and CTA: globaltimer at kernel
-entry, dependency resolved (griddepcontrol.wait), ring fully issued, exit).
+entry, dependency resolved (griddepcontrol.wait), ring fully issued, exit
+after the CTA's epilogue).  Needs a library built with `make TRACE=1`.
 
     RBFFD_TRACE=/tmp/t.bin python bench.py --quick ...; python tools/trace_summary.py /tmp/t.bin
 """
@@ -26,6 +27,7 @@ def summarise(t):
     gap = wait.min(1)[1:] - exit_.max(1)[:-1]  # dependency resolution after the previous step's last CTA
     early = entry.min(1)[1:] - exit_.max(1)[:-1]  # next step's first CTA entry vs this step's end
     prod = issued.max(1) - wait.min(1)
+    drain = (exit_ - issued).mean(1)  # per CTA: last chunk issued -> CTA done
     period = exit_.max(1)[1:] - exit_.max(1)[:-1]
     us = lambda x: f"{np.median(x) / 1e3:7.2f}"
     print(f"steps {S}  CTAs {t.shape[1]}")
@@ -35,6 +37,7 @@ def summarise(t):
     print(f"  dependency gap (last exit -> next first resolved) {us(gap)} us")
     print(f"  next step's first CTA entry vs last exit {us(early)} us (negative: PDL prelaunch)")
     print(f"  producer: ring issued (last CTA) after first resolved {us(prod)} us")
+    print(f"  drain (CTA mean: last chunk issued -> exit) {us(drain)} us")
 
 
 if __name__ == "__main__":
