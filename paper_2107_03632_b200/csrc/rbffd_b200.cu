@@ -478,8 +478,13 @@ int staged_h2d(double* ddst, const double* src, size_t count, cudaStream_t st, i
     const size_t n = std::min(chunk, count - lo);
     RBF_CK(cudaEventSynchronize(sg.ev[b]));  // the previous DMA out of this buffer is done
     double* hb = reinterpret_cast<double*>(sg.buf[b]);
-#pragma omp parallel for schedule(static)
-    for (int64_t e = 0; e < static_cast<int64_t>(n); ++e) hb[e] = src[lo + e];
+#pragma omp parallel
+    {
+      const int64_t T = omp_get_num_threads(), t = omp_get_thread_num();
+      const int64_t a = static_cast<int64_t>(n) * t / T, e = static_cast<int64_t>(n) * (t + 1) / T;
+      copy_f64_nt(hb + a, src + lo + a, e - a);
+      _mm_sfence();
+    }
     RBF_CK(cudaMemcpyAsync(ddst + lo, hb, n * sizeof(double), cudaMemcpyHostToDevice, st));
     RBF_CK(cudaEventRecord(sg.ev[b], st));
   }
@@ -1256,7 +1261,10 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
     RBF_TRY(pool_alloc(&d_int, static_cast<size_t>(std::max<int64_t>(1, N_i)), p->stream));
     RBF_TRY(pool_alloc(&d_seen, static_cast<size_t>(N), p->stream));
     RBF_TRY(pool_alloc(&d_flag, static_cast<size_t>(N), p->stream));
-    RBF_CK(cudaMemcpyAsync(d_int, interior, sizeof(long long) * N_i, cudaMemcpyHostToDevice, p->stream));
+    // 8-byte elements through the pinned staging pair (pageable copies run at
+    // ~11 GB/s and block the host); doubles here are only bit copies
+    RBF_TRY(staged_h2d(reinterpret_cast<double*>(d_int), reinterpret_cast<const double*>(interior),
+                       static_cast<size_t>(N_i), p->stream, device));
     RBF_CK(cudaMemcpyAsync(d_seen, seen.data(), N, cudaMemcpyHostToDevice, p->stream));
     const int blocks = static_cast<int>(std::min<int64_t>((std::max(N, N_i) + 255) / 256, 148 * 16));
     long long* d_order = nullptr;
@@ -1269,7 +1277,7 @@ int plan_create_impl(rbf_plan** out, int64_t N, int64_t N_i, int32_t n, const in
       RBF_TRY(pool_alloc(&d_key, static_cast<size_t>(N_i), p->stream));
       RBF_TRY(pool_alloc(&d_key2, static_cast<size_t>(N_i), p->stream));
       RBF_TRY(pool_alloc(&d_val, static_cast<size_t>(N_i), p->stream));
-      RBF_CK(cudaMemcpyAsync(d_pos, positions, sizeof(double) * 2 * N, cudaMemcpyHostToDevice, p->stream));
+      RBF_TRY(staged_h2d(d_pos, positions, static_cast<size_t>(2 * N), p->stream, device));
       const double sx = (xmax > xmin) ? 2097151.0 / (xmax - xmin) : 0.0;
       const double sy = (ymax > ymin) ? 2097151.0 / (ymax - ymin) : 0.0;
       rbf::morton_keys_kernel<<<blocks, 256, 0, p->stream>>>(d_pos, d_int, N_i, xmin, ymin, sx, sy, d_key, d_val);
