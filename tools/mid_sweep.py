@@ -1,4 +1,4 @@
-"""Mid-size problems: single-step graph loop vs two-step kernel vs dataflow loop (us/step)."""
+"""Mid-size problems: single-step graph loop vs the grid-resident loop (us/step)."""
 import sys
 
 import numpy as np
