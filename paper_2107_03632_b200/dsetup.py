@@ -67,7 +67,11 @@ class RankSetup:
     (``finish``) turns every rank's requests into this rank's send lists."""
 
     def __init__(self, positions: np.ndarray, is_boundary: np.ndarray, n: int, rank: int, world: int,
-                 device: int = 0):
+                 device: int = 0, knn=None, array_device=None):
+        """`knn(positions, n, query_ids) -> (len(query), n) int64` defaults to
+        the device kNN (rbf_knn_subset on `device`); `array_device` (a torch
+        device, default cuda:`device`) holds the index arithmetic.  The CPU
+        tests of the multi-rank logic pass a host kNN and "cpu"."""
         import torch
 
         from .neighborhoods import build_stencils_subset
@@ -76,7 +80,10 @@ class RankSetup:
         self.rank, self.world, self.n = rank, world, n
         positions = np.ascontiguousarray(positions, dtype=np.float64)
         N = positions.shape[0]
-        dev = torch.device("cuda", device)
+        dev = torch.device(array_device) if array_device is not None else torch.device("cuda", device)
+        if knn is None:
+            def knn(pos, nn, query):
+                return build_stencils_subset(pos, nn, query, device=device)
         interior = np.flatnonzero(~np.asarray(is_boundary)).astype(np.int64)
         n_rows = interior.size
         if n_rows < world:
@@ -100,7 +107,7 @@ class RankSetup:
         own_nodes_h = own_nodes.cpu().numpy()
         del perm, int_t
         # exact supports of the own rows only (global ids, host)
-        rows_g = build_stencils_subset(positions, n, own_nodes_h, device=device)
+        rows_g = np.ascontiguousarray(knn(positions, n, own_nodes_h), dtype=np.int64)
         # interior-first row order (multigpu.partition): rows that read no
         # halo value first, each group in Morton order
         reads_halo = np.zeros(rows_g.shape[0], dtype=bool)
@@ -152,7 +159,8 @@ class RankSetup:
         halo_h = halo.cpu().numpy()
         self.l2g = np.concatenate([bnd.cpu().numpy(), halo_h, own_nodes_h]).astype(np.int64)
         del owner, slot, fslot, U, lid_u
-        torch.cuda.empty_cache()
+        if dev.type == "cuda":
+            torch.cuda.empty_cache()
         self.B, self.H = B, H
         self.n_own = own_nodes_h.size
         self._own_sorted = np.argsort(own_nodes_h, kind="stable")
@@ -196,9 +204,10 @@ class RankSetup:
         return part
 
 
-def build_parts_in_process(positions, is_boundary, n, world, device=0):
+def build_parts_in_process(positions, is_boundary, n, world, device=0, knn=None, array_device=None):
     """All ranks' parts in one process (tests, and single-process groups):
     phase 1 for every rank, then the request exchange, then phase 2."""
-    setups = [RankSetup(positions, is_boundary, n, p, world, device) for p in range(world)]
+    setups = [RankSetup(positions, is_boundary, n, p, world, device, knn=knn, array_device=array_device)
+              for p in range(world)]
     reqs = [s.requests for s in setups]
     return setups, [s.finish(reqs) for s in setups]
