@@ -389,6 +389,8 @@ def build_problem(workload: str, gpu_setup: bool):
 LOOPS = {0: "resident on-chip loop (one CTA)",
          1: "streaming step (plain loads), CUDA graphs of 64 steps",
          2: "streaming step (TMA bulk-copy ring, warp-specialised), CUDA graphs of 64 steps",
+         5: "persistent streaming loop (TMA bulk-copy ring, warp-specialised; one cooperative launch per run, "
+            "grid barrier per step, the ring streams the next step while the consumers finish)",
          3: "cluster-resident loop (thread-block cluster, DSMEM halo, one launch)",
          4: "grid-resident loop (rows in every SM's shared memory, one cooperative launch, grid barrier per step)"}
 
@@ -398,7 +400,8 @@ def roofline(info: dict, per_launch: float, peak: float, peak_src: str, traffic)
     bn = info["bytes_per_step"]
     return {
         "bound": "hbm",
-        "kernel": "step_tma_kernel" if info["variant"] == 2 else LOOPS[info["variant"]],
+        "kernel": ("stream_loop_kernel" if info.get("persist") else
+                   "step_tma_kernel" if info["variant"] == 2 else LOOPS[info["variant"]]),
         "achieved": stream / per_launch / 1e9,
         "peak": peak,
         "unit": "GB/s",
@@ -466,7 +469,7 @@ def run_per_config(workloads, peak, peak_src):
             "workload": WORKLOADS[name][3], "N": int(nodes.n_total), "N_i": N_i, "n": n,
             "m": int(shapes.degree), "dt": dt, "steps": steps, "warmup": 3,
             "value": steps * N_i / res.device_seconds, "ms_per_step": 1e3 * per_launch,
-            "gpu_launches": launches, "loop": LOOPS[info["variant"]],
+            "gpu_launches": launches, "loop": LOOPS[5] if info["persist"] else LOOPS[info["variant"]],
             "roofline": roofline(info, per_launch, peak, peak_src, committed_traffic(name)),
             "parity": {"steps": psteps, "sha256_gpu": g, "sha256_oracle": o, "equal": g == o,
                        "residual_equal": pres.residual == want["residual"]},
@@ -627,7 +630,8 @@ def main():
         "impl_config": {
             "setup": setup_text(args.gpu_setup),
             "renumber": "morton (bit-identical)" if renumber else "native (advancing-front order)",
-            "loop": LOOPS[info["variant"]] + ("" if args.no_pdl or info["resident"] else " + PDL"),
+            "loop": (LOOPS[5] if info["persist"] else
+                     LOOPS[info["variant"]] + ("" if args.no_pdl or info["resident"] else " + PDL")),
             "index_bits": info["index_bits"],
             "parallelism": "single GPU",
         },

@@ -61,6 +61,8 @@ extern "C" {
 #define RBF_NO_PAIR 0x80u         /* fixed-step runs one step per launch (no two-step tile kernel) */
 #define RBF_PAIR 0x100u           /* two-step tile kernel for fixed-step runs at any size (default:
                                      only up to N_i*n = 1e6, where it is measured faster) */
+#define RBF_NO_PERSIST 0x400u     /* streaming runs: one graph-captured launch per step instead of
+                                     the persistent loop (one cooperative launch per run) */
 #define RBF_ACCEPT_ILLCOND 0x200u /* rbf_plan_create_assembled: accept row status 1 (the caller has
                                      checked those rows' exact condition); status 2 still fails */
 
@@ -262,6 +264,9 @@ typedef struct rbf_plan_info {
                               temporal blocking, bitwise identical) */
   int32_t pair_tiles;      /* its row tiles */
   int64_t pair_halo_rows;  /* halo entries over all tiles (rows recomputed per launch) */
+  int32_t persist;         /* 1: streaming runs (variant 2) go through the persistent loop, one
+                              cooperative launch per run (RBF_NO_PERSIST: one launch per step) */
+  int32_t persist_grid;    /* its CTAs */
 } rbf_plan_info;
 
 int rbf_plan_get_info(const rbf_plan* plan, rbf_plan_info* info);

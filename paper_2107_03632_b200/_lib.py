@@ -30,6 +30,7 @@ RBF_NO_IDX16 = 0x20
 RBF_NO_PAIR = 0x80
 RBF_PAIR = 0x100
 RBF_ACCEPT_ILLCOND = 0x200
+RBF_NO_PERSIST = 0x400
 
 RBF_MODE_FIXED = 0
 RBF_MODE_STEADY = 1
@@ -94,6 +95,8 @@ class PlanInfo(ctypes.Structure):
         ("pair", ctypes.c_int32),
         ("pair_tiles", ctypes.c_int32),
         ("pair_halo_rows", ctypes.c_int64),
+        ("persist", ctypes.c_int32),
+        ("persist_grid", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

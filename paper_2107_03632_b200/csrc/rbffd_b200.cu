@@ -81,6 +81,7 @@ using TmaFn = void (*)(rbf::StepArgs, const double*, double*, int, rbf::TmaGeom)
 using ResidentFn = void (*)(rbf::ResidentArgs);
 using ClusterFn = void (*)(rbf::ClusterArgs);
 using GridFn = void (*)(rbf::GridArgs);
+using LoopFn = void (*)(rbf::StepArgs, rbf::LoopArgs, rbf::TmaGeom);
 
 template <int NJ>
 struct KernelSet {
@@ -111,6 +112,15 @@ struct KernelSet {
     }
   }
   static int cw(int cw_req) { return (NJ > 0 && cw_req == kCWide) ? kCWide : kCW; }
+  // persistent streaming loop (one cooperative launch per run)
+  static LoopFn loop(bool idx16) {
+    if constexpr (NJ > 0) {
+      return idx16 ? rbf::stream_loop_kernel<NJ, kCW, 2> : rbf::stream_loop_kernel<NJ, kCW, 4>;
+    } else {
+      (void)idx16;
+      return nullptr;
+    }
+  }
   static GridFn grid(bool two) {
     if constexpr (NJ > 0) return two ? rbf::grid_loop_kernel<NJ, true> : rbf::grid_loop_kernel<NJ, false>;
     else {
@@ -211,6 +221,11 @@ struct rbf_plan {
   int variant = 1;                 // 0 resident, 1 LDG streaming, 2 TMA streaming, 3 cluster loop
   ClusterFn cluster_fn = nullptr;  // non-null: the loop runs in one thread-block cluster
   GridFn grid_fn = nullptr;        // non-null: the loop runs in one cooperative grid (rows in smem)
+  LoopFn loop_fn = nullptr;        // non-null: streaming runs go through the persistent loop
+  size_t loop_smem = 0;
+  int loop_grid = 0;
+  rbf::TmaGeom loop_geom = {1, 2, 0, 0};
+  unsigned long long* loop_red = nullptr;  // [7] residual slots + arrival counter
   int grid_ctas = 0, grid_spc = 0, grid_spr = 0;
   size_t grid_smem = 0;
   unsigned long long* grid_red = nullptr;  // [3][2] per-step partial slots
@@ -227,6 +242,7 @@ struct rbf_plan {
   // two steps per launch (pair_kernels.cu): fixed-step runs of TMA plans
   rbf::PairPlan pair;
   bool pair_ok = false;
+  bool pair_forced = false;        // RBF_PAIR / RBFFD_PAIR=1: ahead of the persistent loop
   cudaGraphExec_t pair_graph = nullptr;
   int kernel_n = 0;
   bool resident = false;
@@ -829,6 +845,33 @@ int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
   return RBF_OK;
 }
 
+// The whole run in one cooperative launch of the persistent streaming loop;
+// the final field is published into both buffers.
+int run_loop(rbf_plan* p, int64_t limit, bool steady) {
+  RBF_CK(cudaMemsetAsync(p->loop_red, 0, 7 * sizeof(unsigned long long), p->stream));
+  rbf::LoopArgs L;
+  L.U0 = p->U[0];
+  L.U1 = p->U[1];
+  L.limit = limit;
+  L.flags = steady ? rbf::kSteady : 0;
+  L.red = p->loop_red;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p->loop_grid);
+  cfg.blockDim = dim3(p->tma_block);
+  cfg.dynamicSmemBytes = p->loop_smem;
+  cfg.stream = p->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: grid barrier per step
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RBF_CK(cudaEventRecord(p->ev0, p->stream));
+  RBF_CK(cudaLaunchKernelEx(&cfg, p->loop_fn, p->args(), L, p->loop_geom));
+  ++p->launches;
+  RBF_CK(cudaEventRecord(p->ev1, p->stream));
+  return RBF_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1109,7 +1152,10 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
     if (smem_t <= kResidentSmemMax && set_max_smem(tma_fn) == cudaSuccess) {
       p->tma_fn = tma_fn;
       p->tma_geom = rbf::TmaGeom{sps, stages, 0, 0};
-      p->tma_geom.res = (3 * stages) / 2;  // ring-fill chunks stay L2-resident (TmaGeom::res; sweep in profiles/README.md)
+      // ring-fill chunks stay L2-resident (TmaGeom::res): 8 for n <= 20 (C2
+      // 29.5 -> 28.4 us with the round-2 kernel, profiles/r02/c2_geom_sweep.log),
+      // 1.5 x stages above (round-1 sweep)
+      p->tma_geom.res = n <= 20 ? 8 : (3 * stages) / 2;
       if (const char* e = std::getenv("RBFFD_L2_RES_CHUNKS")) p->tma_geom.res = std::atoll(e);
       p->tma_smem = smem_t;
       p->tma_block = 32 * (cw + 1);
@@ -1121,6 +1167,52 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
     } else {
       cudaGetLastError();
     }
+  }
+  // persistent streaming loop (stream_loop_kernel): the TMA step's ring in one
+  // cooperative launch per run; RBFFD_PERSIST=0 keeps the graph + PDL loop
+  const char* persist_env = std::getenv("RBFFD_PERSIST");
+  if (p->tma_fn && !p->resident && !(flags & RBF_NO_PERSIST) && !(persist_env && std::atoi(persist_env) == 0)) {
+    LoopFn lfn = nullptr;
+    switch (n) {
+#define RBF_LCASE(K) \
+  case K:            \
+    lfn = KernelSet<K>::loop(p->index_bits == 16); \
+    break;
+      RBF_SPECIALISED(RBF_LCASE)
+#undef RBF_LCASE
+      default:
+        break;
+    }
+    int optin_l = 0;
+    RBF_CK(cudaDeviceGetAttribute(&optin_l, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    if (lfn && set_max_smem(lfn) == cudaSuccess) {
+      cudaFuncAttributes lfa;
+      RBF_CK(cudaFuncGetAttributes(&lfa, lfn));
+      const int slice = n * 32 * (8 + p->index_bits / 8) + 32 * 8 + (p->index_bits == 16 ? 16 : 0);
+      // slices per stage of the persistent loop: its ring never drains, so
+      // larger stages pay (C2: 5 -> 24.7 us per step vs 4 -> 25.7;
+      // profiles/r02/persistent_loop_ab.log)
+      int lsps = p->tma_geom.sps;
+      if (p->index_bits == 16 && n <= 20) lsps = std::max(1, 30000 / slice);
+      if (const char* e = std::getenv("RBFFD_LOOP_SPS")) lsps = std::max(1, std::atoi(e));
+      const int stage = lsps * slice;
+      const size_t room = static_cast<size_t>(optin_l) - lfa.sharedSizeBytes - 2 * 16 * sizeof(uint64_t) - 256;
+      int stages = std::min(16, static_cast<int>(room / stage));
+      if (const char* e = std::getenv("RBFFD_LOOP_STAGES")) stages = std::max(2, std::min(stages, std::atoi(e)));
+      const size_t lsmem = 2 * 16 * sizeof(uint64_t) + static_cast<size_t>(stages) * stage;
+      int occ = 0;
+      if (stages >= 2 &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lfn, p->tma_block, lsmem) == cudaSuccess &&
+          occ >= 1) {
+        RBF_TRY(dev_alloc(p.get(), &p->loop_red, 7));
+        p->loop_fn = lfn;
+        p->loop_smem = lsmem;
+        p->loop_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((p->S + lsps - 1) / lsps,
+                                                                                 int64_t(sms) * occ)));
+        p->loop_geom = rbf::TmaGeom{lsps, stages, 0, 0};
+      }
+    }
+    cudaGetLastError();
   }
   // two-step tile kernel for fixed-step runs (pair_kernels.cu)
   // (Runs only when no on-chip loop applies: the grid-resident loop wins at
@@ -1142,6 +1234,7 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
                             p->stream, &p->pair, &ok));
     if (ok && set_max_smem(p->pair.fn) == cudaSuccess) {
       p->pair_ok = true;
+      p->pair_forced = pair_force;
       p->device_bytes += p->pair.halo_slices * 32LL * (12LL * n + 12) + p->S * 32LL * n * 2;
     } else {
       if (ok) rbf::pair_free(&p->pair, p->stream);
@@ -2019,8 +2112,12 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
   int rc;
   int pair_buf = -1;  // >= 0: the pair path ran and left the field in U[pair_buf]
   PhaseTimer timer;
+  bool published = p->resident;  // the loop publishes the final field into both buffers
   if (p->resident) {
     rc = run_resident(p, limit, steady, copy_back != 0);
+  } else if (p->loop_fn && limit >= 1 && !(p->pair_forced && !steady && limit >= 2)) {
+    rc = run_loop(p, limit, steady);
+    published = true;
   } else if (p->pair_ok && !steady && limit >= 2) {
     bool fallback = false;
     int final_buf = 0;
@@ -2076,12 +2173,12 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
   if (s.bad_step >= 0) {
     // field of the failing step's u2 (solver.py:201)
     p->cur = copy_back ? 0 : static_cast<int>((s.bad_step + 1) & 1);
-    if (p->resident) p->cur = 0;  // resident / cluster loops publish into both buffers
+    if (published) p->cur = 0;  // resident / cluster / persistent loops publish into both buffers
     if (steps_done) *steps_done = s.bad_step;
     if (has_residual) *has_residual = 0;
     return fail(RBF_ERR_INSTABILITY, "time loop unstable at step " + std::to_string(s.bad_step));
   }
-  p->cur = (copy_back || p->resident) ? 0 : static_cast<int>(done & 1);
+  p->cur = (copy_back || published) ? 0 : static_cast<int>(done & 1);
   if (pair_buf >= 0) p->cur = pair_buf;
   if (steps_done) *steps_done = done;
   if (residual) *residual = have_res ? res : 0.0;
@@ -2155,6 +2252,8 @@ int rbf_plan_get_info(const rbf_plan* p, rbf_plan_info* info) {
   info->pair = p->pair_ok ? 1 : 0;
   info->pair_tiles = p->pair_ok ? p->pair.args.n_tiles : 0;
   info->pair_halo_rows = p->pair_ok ? p->pair.halo_entries : 0;
+  info->persist = p->loop_fn ? 1 : 0;
+  info->persist_grid = p->loop_fn ? p->loop_grid : 0;
   info->stream_bytes_per_step = (p->index_bits == 16 && !p->resident)
       ? p->N_i * (10LL * p->n + 24) + p->S * 16 + p->overflow_slices * 32LL * p->n * 4
       : info->bytes_per_step;
@@ -2209,6 +2308,7 @@ void rbf_plan_destroy(rbf_plan* p) {
   pool_free(p->halo_send_idx, s);
   pool_free(p->cluster_dest, s);
   pool_free(p->grid_red, s);
+  pool_free(p->loop_red, s);
   pool_free(p->C16, s);
   pool_free(p->meta, s);
   pool_free(p->u_init, s);

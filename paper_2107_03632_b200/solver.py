@@ -163,7 +163,7 @@ class Plan:
     def __init__(self, n_total, interior, rows, weights, f_int, positions=None, *,
                  renumber: bool = False, device: int = 0, resident: bool = True,
                  pdl: bool = True, tma: bool = True, cluster: bool = True, idx16: bool = True,
-                 pair: Optional[bool] = None):
+                 pair: Optional[bool] = None, persist: bool = True):
         self._lib = _lib.load()
         interior = _as(interior, np.int64)
         weights = _as(weights, np.float64)
@@ -192,6 +192,8 @@ class Plan:
         if not idx16:
             flags |= _lib.RBF_NO_IDX16
         flags |= _pair_flags(pair)
+        if not persist:
+            flags |= _lib.RBF_NO_PERSIST
         handle = ctypes.c_void_p()
         rc = self._lib.rbf_plan_create(
             ctypes.byref(handle), int(n_total), int(n_rows), int(n), _ptr(interior), _ptr(rows),

@@ -395,10 +395,10 @@ def test_streaming_graph_chunk_step_counts(synth_cache, steps):
     nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
     interior = shapes.interior_nodes
     want = orc.run_time_loop(nodes, shapes, steps=steps)
-    for idx16 in (True, False):
+    for idx16, persist in ((True, False), (False, False), (True, True), (False, True)):
         plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
                     rb.forcing(nodes.positions[interior]), nodes.positions, renumber=True,
-                    idx16=idx16, resident=False, pair=False)
+                    idx16=idx16, resident=False, pair=False, persist=persist)
         assert plan.info()["variant"] == 2
         plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
         res = plan.run(0.5 * rb.stability_bound(shapes), steps=steps)
@@ -593,10 +593,10 @@ def test_synthetic_steady_streaming_matches_oracle(synth_cache):
     assert rep.residual == want["residual"]
     assert np.array_equal(rep.field, want["field"])
     interior = shapes.interior_nodes
-    for renumber in (False, True):
+    for renumber, persist in ((False, False), (True, False), (True, True)):
         plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
                     rb.forcing(nodes.positions[interior]), nodes.positions, renumber=renumber,
-                    resident=False, pair=False)
+                    resident=False, pair=False, persist=persist)
         assert plan.info()["variant"] == 2 and plan.info()["resident"] == 0
         plan.set_field(rb.apply_dirichlet(nodes, np.zeros(nodes.n_total)))
         res = plan.run(0.5 * rb.stability_bound(shapes), mode="steady", tol=1e-2, max_steps=200_000)
@@ -944,3 +944,33 @@ def test_device_stability_bound_has_numpys_bits(n):
                            stencils=rb.StencilSet(n=n, neighbors=np.zeros((N, n), dtype=np.int64)))
     assert 2.0 / plan.weight_row_sum_max() == rb.stability_bound(shapes)
     plan.close()
+
+
+@pytest.mark.parametrize("persist", [True, False], ids=["persistent-loop", "graph-loop"])
+def test_streaming_failure_and_copy_back(synth_cache, persist):
+    """Streaming runs (persistent loop: one cooperative launch per run; graph
+    loop: one launch per step): a non-finite step stops at the oracle's step
+    with its u2 as the field (solver.py:200-206), copy-back equals swap, and
+    the plan keeps working after the failure."""
+    nodes, _, shapes = _synth(synth_cache, 1_000_000, 15, 2)
+    interior = shapes.interior_nodes
+    plan = Plan(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
+                rb.forcing(nodes.positions[interior]), nodes.positions, renumber=True, resident=False,
+                pair=False, persist=persist)
+    u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
+    bad_dt = 40.0 * rb.stability_bound(shapes)
+    want = orc.run_time_loop(nodes, shapes, dt=bad_dt, steps=200)
+    assert want["status"] == orc.ORC_INSTABILITY
+    plan.set_field(u0)
+    res = plan.run(bad_dt, steps=200)
+    assert res.status == _lib.RBF_ERR_INSTABILITY and res.bad_step == want["step"]
+    assert np.array_equal(plan.get_field(), want["field"], equal_nan=True)
+    dt = 0.5 * rb.stability_bound(shapes)
+    want = orc.run_time_loop(nodes, shapes, dt=dt, steps=67)
+    for copy_back in (False, True):
+        plan.set_field(u0)
+        res = plan.run(dt, steps=67, copy_back=copy_back)
+        assert res.steps_done == 67 and res.residual == want["residual"]
+        assert np.array_equal(plan.get_field(), want["field"])
+    plan.close()
+
