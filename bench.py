@@ -413,6 +413,9 @@ def roofline(info: dict, per_launch: float, peak: float, peak_src: str, traffic)
                           if info["index_bits"] == 16 else
                           "N_i*(12n+24): 8n w + 4n ids + 8 f + 8 u_self + 8 u_out"),
         "peak_source": peak_src,
+        "per": ("step: the persistent loop runs all K steps in one launch; achieved = K x bytes_per_launch "
+                "/ that launch's event time, traffic = ncu DRAM bytes of one launch / its steps"
+                if info.get("persist") else "launch (one step)"),
         "index_bits": info["index_bits"],
         "Bn_bytes_per_launch": bn,
         "Bn_equivalent_GBps": bn / per_launch / 1e9,

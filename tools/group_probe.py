@@ -21,11 +21,17 @@ f = rb.forcing(nodes.positions[interior])
 u0 = rb.apply_dirichlet(nodes, np.zeros(nodes.n_total))
 dt = 0.5 * rb.stability_bound(sh)
 steps = 2000
-plan = rb.Plan(nodes.n_total, interior, rows, sh.weights, f, nodes.positions, renumber=True, pair=False)
-plan.set_field(u0)
-plan.run(dt, steps=100)
-t1 = min(plan.run(dt, steps=steps).device_seconds for _ in range(3)) / steps
-print(f"N={nodes.n_total} one plan: {1e6 * t1:.2f} us/step", flush=True)
+for persist in (False, True):
+    plan = rb.Plan(nodes.n_total, interior, rows, sh.weights, f, nodes.positions, renumber=True, pair=False,
+                   persist=persist)
+    plan.set_field(u0)
+    plan.run(dt, steps=100)
+    t = min(plan.run(dt, steps=steps).device_seconds for _ in range(3)) / steps
+    print(f"N={nodes.n_total} one plan ({'persistent loop' if persist else 'graph loop'}): "
+          f"{1e6 * t:.2f} us/step", flush=True)
+    if not persist:
+        t1 = t  # the parts run the graph loop: compare like with like
+    del plan
 for P in (2, 4):
     parts = partition(nodes.n_total, interior, rows, sh.weights, f, nodes.positions, P)
     for push in (True, False):
