@@ -1190,10 +1190,11 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
       RBF_CK(cudaFuncGetAttributes(&lfa, lfn));
       const int slice = n * 32 * (8 + p->index_bits / 8) + 32 * 8 + (p->index_bits == 16 ? 16 : 0);
       // slices per stage of the persistent loop: its ring never drains, so
-      // larger stages pay (C2: 5 -> 24.7 us per step vs 4 -> 25.7;
-      // profiles/r02/persistent_loop_ab.log)
+      // larger stages pay (C2: 5 -> 24.7 us per step vs 4 -> 25.7; C4: 2 ->
+      // 2.592 ms vs 1 -> 2.707; profiles/r02/loop_geom_sweep.log)
       int lsps = p->tma_geom.sps;
       if (p->index_bits == 16 && n <= 20) lsps = std::max(1, 30000 / slice);
+      if (p->index_bits == 32) lsps = std::max(1, 45000 / slice);
       if (const char* e = std::getenv("RBFFD_LOOP_SPS")) lsps = std::max(1, std::atoi(e));
       const int stage = lsps * slice;
       const size_t room = static_cast<size_t>(optin_l) - lfa.sharedSizeBytes - 2 * 16 * sizeof(uint64_t) - 256;

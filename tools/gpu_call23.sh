@@ -2,6 +2,7 @@
 # in-process group probe, ncu launch list and --set full of stream_loop_kernel.
 set -x
 OUT=gpurun_out
+timeout 300 python bench.py --workload c4 --gpu-setup --quick --steps 40 --warmup 10 > $OUT/r2_c4_default.json 2>/dev/null; echo c4=$?
 timeout 900 python bench.py --steps 20 --warmup 5 > $OUT/r2_bench.json 2> $OUT/r2_bench.err; echo bench=$?
 timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > $OUT/r2_ref.json 2> $OUT/r2_ref.err; echo ref=$?
 timeout 600 python tools/group_probe.py 2e6 > $OUT/r2_group_probe.log 2>&1; echo group=$?
