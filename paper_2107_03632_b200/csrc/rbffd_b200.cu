@@ -1244,8 +1244,9 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
   }
   if (p->tma_fn && std::getenv("RBFFD_TRACE")) {  // diagnostics: CTA timelines of up to 4096 steps
     p->trace_cap = 4096;
-    RBF_TRY(dev_alloc(p.get(), &p->trace, static_cast<size_t>(p->trace_cap) * p->grid * 4));
-    RBF_CK(cudaMemsetAsync(p->trace, 0, sizeof(unsigned long long) * p->trace_cap * p->grid * 4, p->stream));
+    const int tg = std::max(p->grid, p->loop_grid);
+    RBF_TRY(dev_alloc(p.get(), &p->trace, static_cast<size_t>(p->trace_cap) * tg * 4));
+    RBF_CK(cudaMemsetAsync(p->trace, 0, sizeof(unsigned long long) * p->trace_cap * tg * 4, p->stream));
   }
   if (!p->tma_fn) {
     RBF_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p->stream_fn, kStreamBlock, 0));
@@ -2114,11 +2115,13 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
   int pair_buf = -1;  // >= 0: the pair path ran and left the field in U[pair_buf]
   PhaseTimer timer;
   bool published = p->resident;  // the loop publishes the final field into both buffers
+  bool looped = false;            // the persistent streaming loop ran
   if (p->resident) {
     rc = run_resident(p, limit, steady, copy_back != 0);
   } else if (p->loop_fn && limit >= 1 && !(p->pair_forced && !steady && limit >= 2)) {
     rc = run_loop(p, limit, steady);
     published = true;
+    looped = true;
   } else if (p->pair_ok && !steady && limit >= 2) {
     bool fallback = false;
     int final_buf = 0;
@@ -2145,10 +2148,11 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
   const rbf::DevStatus s = *p->h_st;
   if (p->trace && limit > 0) {  // RBFFD_TRACE: append {grid, steps, [steps][grid][4] ns} to the file
     const int64_t n_tr = std::min<int64_t>(limit, p->trace_cap);
-    std::vector<unsigned long long> h(static_cast<size_t>(n_tr) * p->grid * 4);
+    const int tg = looped ? p->loop_grid : p->grid;
+    std::vector<unsigned long long> h(static_cast<size_t>(n_tr) * tg * 4);
     RBF_CK(cudaMemcpy(h.data(), p->trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     if (std::FILE* f = std::fopen(std::getenv("RBFFD_TRACE"), "ab")) {
-      const int64_t hdr[2] = {p->grid, n_tr};
+      const int64_t hdr[2] = {looped ? -tg : tg, n_tr};  // negative: persistent-loop layout
       std::fwrite(hdr, sizeof(hdr), 1, f);
       std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
       std::fclose(f);

@@ -407,12 +407,22 @@ stream_loop_kernel(StepArgs a, LoopArgs L, TmaGeom g) {
     const bool need = steady || step == L.limit - 1;
     bool bad = false;
     unsigned long long dmax = 0ull;
+#ifdef RBF_TRACE
+    unsigned long long tr0 = 0;
+    if (a.trace && ctid == 0) tr0 = globaltimer();
+#endif
+    // ring position of chunk q = step * my_n + i: one 64-bit division per
+    // step, 32-bit arithmetic per unit (a 64-bit div/mod is a SASS subroutine)
     const long long qbase = step * my_n;
+    const long long qdiv = qbase / stages;
+    const int qmod = static_cast<int>(qbase - qdiv * stages);
+    const uint32_t qpar = static_cast<uint32_t>(qdiv & 1);
     for (int uq = warp - 1; uq < my_n * upc; uq += CW) {
       const int i = uq / upc, slot = uq - i * upc;
       const long long q = qbase + i;
-      const int s = static_cast<int>(q % stages);
-      const uint32_t ph = static_cast<uint32_t>((q / stages) & 1);
+      const int t = qmod + i, tdiv = t / stages;
+      const int s = t - tdiv * stages;
+      const uint32_t ph = (qpar + static_cast<uint32_t>(tdiv)) & 1u;
       if (lane == 0) {
         while (*reinterpret_cast<volatile long long*>(&s_issued) <= q) __nanosleep(64);
       }
@@ -474,6 +484,10 @@ stream_loop_kernel(StepArgs a, LoopArgs L, TmaGeom g) {
     }
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
     const int rs = static_cast<int>(step % 3);
+#ifdef RBF_TRACE
+    unsigned long long tr1 = 0;
+    if (a.trace && ctid == 0) tr1 = globaltimer();
+#endif
     if (ctid == 0) {
       unsigned int cbad = 0;
       unsigned long long cm = 0ull;
@@ -496,6 +510,15 @@ stream_loop_kernel(StepArgs a, LoopArgs L, TmaGeom g) {
       // flag bits are this barrier's only at the exact count (a CTA already
       // past it has passed a clean barrier: a flagged one stops every CTA)
       s_seen = ((v & kCount) == target) ? v : 0ull;
+#ifdef RBF_TRACE
+      if (a.trace) {  // per step and CTA: start, arrival, release, chunks armed at arrival
+        unsigned long long* o = a.trace + ((step % a.trace_cap) * gridDim.x + blockIdx.x) * 4;
+        o[0] = tr0;
+        o[1] = tr1;
+        o[2] = globaltimer();
+        o[3] = static_cast<unsigned long long>(*reinterpret_cast<volatile long long*>(&s_issued) - (step + 1) * my_n);
+      }
+#endif
     }
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
     // the reference checks every step's flag before its residual (solver.py:200-217)

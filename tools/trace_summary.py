@@ -13,10 +13,27 @@ def runs(path):
     raw = np.fromfile(path, dtype=np.uint64)
     i = 0
     while i < raw.size:
-        G, S = int(raw[i]), int(raw[i + 1])
+        G, S = int(raw[i].astype(np.int64)), int(raw[i + 1])
         i += 2
-        yield raw[i:i + G * S * 4].reshape(S, G, 4).astype(np.int64)
-        i += G * S * 4
+        g = abs(G)
+        yield G < 0, raw[i:i + g * S * 4].reshape(S, g, 4).astype(np.int64)
+        i += g * S * 4
+
+
+def summarise_loop(t):
+    """Persistent loop (header grid < 0): per step and CTA: consumers start,
+    CTA arrival at the grid barrier, release seen, chunks armed ahead."""
+    S = t.shape[0]
+    start, arr, rel, ahead = t[:, :, 0], t[:, :, 1], t[:, :, 2], t[:, :, 3]
+    us = lambda x: f"{np.median(x) / 1e3:7.2f}"
+    print(f"steps {S}  CTAs {t.shape[1]}  (persistent loop)")
+    print(f"  period (last release to last release)     {us(np.diff(rel.max(1)))} us")
+    print(f"  CTA work (start -> arrival), mean / max   {us((arr - start).mean(1))} / {us((arr - start).max(1))} us")
+    print(f"  arrival spread (first -> last CTA)        {us(arr.max(1) - arr.min(1))} us")
+    print(f"  barrier (last arrival -> first release)   {us(rel.min(1) - arr.max(1))} us")
+    print(f"  release spread (first -> last CTA)        {us(rel.max(1) - rel.min(1))} us")
+    print(f"  CTA idle at the barrier, mean             {us((rel - arr).mean(1))} us")
+    print(f"  next-step chunks armed at arrival, mean   {np.median(ahead.mean(1)):7.2f}")
 
 
 def summarise(t):
@@ -41,7 +58,7 @@ def summarise(t):
 
 
 if __name__ == "__main__":
-    for k, t in enumerate(runs(sys.argv[1])):
+    for k, (loop, t) in enumerate(runs(sys.argv[1])):
         print(f"== run {k}")
         if t.shape[0] > 2:
-            summarise(t[1:])  # the first step has no predecessor
+            (summarise_loop if loop else summarise)(t[1:])  # the first step has no predecessor
