@@ -553,6 +553,13 @@ def main():
         torch.cuda.synchronize()
         res, launches = time_plan(plan, dt, args.steps, args.warmup, u0)  # CUDA events, plan stream
         torch.cuda.synchronize()
+        # median and min of 5 more timed runs of the same K steps
+        # (reported beside `value`, which is the single run above)
+        reps = []
+        for _ in range(5):
+            plan.set_field(u0)
+            reps.append(plan.run(dt, steps=args.steps).device_seconds / args.steps)
+        torch.cuda.synchronize()
         # keep the GPU busy a little longer so the sampler sees the load (not counted)
         if res.device_seconds < 1.0 and not args.quick:
             extra = int(min(200_000, max(1, args.steps * (1.0 / max(res.device_seconds, 1e-6)))))
@@ -582,7 +589,7 @@ def main():
     # ---- end to end through the public API (host arrays in, host field out)
     cfg = rb.SolveConfig(degree=int(shapes.degree), support_size=n, nodes=int(nodes.n_total),
                          dt=dt, steps=args.steps)
-    t_e2e = float("nan")
+    t_e2e = t_plan = float("nan")
     if not args.quick:
         rb.run_time_loop(cfg, nodes, shapes, renumber=renumber)  # warm (module load, pools)
         torch.cuda.synchronize()
@@ -591,6 +598,13 @@ def main():
         torch.cuda.synchronize()
         t_e2e = time.perf_counter() - te
         log(f"e2e: {t_e2e * 1e3:.1f} ms (device loop {rep.device_seconds * 1e3:.2f} ms)")
+        # the plan upload alone (reported separately): host arrays -> packed device plan
+        torch.cuda.synchronize()
+        tp = time.perf_counter()
+        Plan(nodes.n_total, interior, rows, shapes.weights, f_int,
+             nodes.positions if renumber else None, renumber=renumber, device=local).close()
+        torch.cuda.synchronize()
+        t_plan = time.perf_counter() - tp
     e2e_value = args.steps * N_i / t_e2e
     N = nodes.n_total
     # bytes copied per call: weights, int32 ids (converted in the staging
@@ -642,7 +656,11 @@ def main():
         "e2e": {"value": e2e_value if math.isfinite(e2e_value) else None, "unit": "node-updates/s",
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                 "what": "run_time_loop(config, nodes, shapes) from host numpy arrays: plan build + H2D "
-                        "(weights, ids, forcing, positions, field), K steps, D2H field, error norms"},
+                        "(weights, ids, forcing, positions, field), K steps, D2H field, error norms",
+                "plan_upload_ms": 1e3 * t_plan if math.isfinite(t_plan) else None},
+        "timing_repeats": {"runs": len(reps), "steps_each": args.steps,
+                           "median_ms_per_step": 1e3 * statistics.median(reps),
+                           "min_ms_per_step": 1e3 * min(reps)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "setup_seconds": t_setup,

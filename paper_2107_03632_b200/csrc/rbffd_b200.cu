@@ -224,7 +224,6 @@ struct rbf_plan {
   LoopFn loop_fn = nullptr;        // non-null: streaming runs go through the persistent loop
   size_t loop_smem = 0;
   int loop_grid = 0;
-  bool loop_slots = true;  // persistent loop: slot barrier (else the arrival counter)
   rbf::TmaGeom loop_geom = {1, 2, 0, 0};
   unsigned long long* loop_red = nullptr;  // [7] residual slots + arrival counter
   int grid_ctas = 0, grid_spc = 0, grid_spr = 0;
@@ -849,10 +848,8 @@ int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
 // The whole run in one cooperative launch of the persistent streaming loop;
 // the final field is published into both buffers.
 int run_loop(rbf_plan* p, int64_t limit, bool steady) {
-  RBF_CK(cudaMemsetAsync(p->loop_red, 0, (7 + 4 * static_cast<size_t>(p->loop_grid)) * sizeof(unsigned long long),
-                         p->stream));
+  RBF_CK(cudaMemsetAsync(p->loop_red, 0, 7 * sizeof(unsigned long long), p->stream));
   rbf::LoopArgs L;
-  L.slots = p->loop_slots ? p->loop_red + 7 : nullptr;
   L.U0 = p->U[0];
   L.U1 = p->U[1];
   L.limit = limit;
@@ -1208,11 +1205,7 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
       if (stages >= 2 &&
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lfn, p->tma_block, lsmem) == cudaSuccess &&
           occ >= 1) {
-        // [0..6]: counter barrier; then 4 x grid words of the slot barrier
-        const int64_t lgrid = std::max<int64_t>(1, std::min<int64_t>((p->S + lsps - 1) / lsps, int64_t(sms) * occ));
-        RBF_TRY(dev_alloc(p.get(), &p->loop_red, static_cast<size_t>(7 + 4 * lgrid)));
-        p->loop_slots = true;
-        if (const char* e = std::getenv("RBFFD_LOOP_BARRIER")) p->loop_slots = std::strcmp(e, "counter") != 0;
+        RBF_TRY(dev_alloc(p.get(), &p->loop_red, 7));
         p->loop_fn = lfn;
         p->loop_smem = lsmem;
         p->loop_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((p->S + lsps - 1) / lsps,

@@ -302,10 +302,6 @@ struct LoopArgs {
   long long limit;             // steps to run (fixed: steps, steady: max_steps)
   int flags;                   // kSteady
   unsigned long long* red;     // [0..2] residual slots, [6] arrival counter
-  // non-null: per-CTA arrival words instead of the counter -- slots[p*G + b]
-  // = step + 1 (| kBad) for step parity p, slots[2G + p*G + b] = the CTA's
-  // residual max; no atomics, every CTA reduces the G words itself
-  unsigned long long* slots;
 };
 
 template <int NJ, int CW, int IB>
@@ -495,69 +491,7 @@ stream_loop_kernel(StepArgs a, LoopArgs L, TmaGeom g) {
     unsigned long long tr1 = 0;
     if (a.trace && ctid == 0) tr1 = globaltimer();
 #endif
-    if (L.slots) {
-      // slot barrier: consumer warp 1 publishes the CTA's word, then its 32
-      // lanes poll the G words of this step's parity.  A CTA past barrier k
-      // writes parity (k+1)&1; parity k&1 is rewritten only after barrier
-      // k+1, which needs this CTA's arrival: the words read here are step k's
-      if (warp == 1) {
-        const int G = gridDim.x;
-        unsigned long long* arr = L.slots + (step & 1) * G;
-        unsigned long long* dmx = L.slots + 2 * G + (step & 1) * G;
-        const unsigned long long target = static_cast<unsigned long long>(step + 1);
-        if (lane == 0) {
-          unsigned int cbad = 0;
-          unsigned long long cm = 0ull;
-          for (int w = 1; w <= CW; ++w) {
-            cbad |= s_bad[w];
-            cm = s_max[w] > cm ? s_max[w] : cm;
-          }
-          if (need) dmx[blockIdx.x] = cm;
-          __threadfence();  // this CTA's field stores and residual before its word
-          const unsigned long long word = target | (cbad ? kBad : 0ull);
-          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(arr + blockIdx.x), "l"(word) : "memory");
-        }
-        unsigned long long orb = 0ull, gm = 0ull;
-        const unsigned long long t0 = globaltimer();
-        // relaxed polls, then one acquire fence (an acquire load per poll
-        // would invalidate L1 on every iteration)
-        for (int k = lane; k < G; k += 32) {
-          unsigned long long v;
-          for (int spin = 0;; ++spin) {
-            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(arr + k) : "memory");
-            if ((v & kCount) >= target) break;
-            if ((spin & 1023) == 1023 && globaltimer() - t0 > 20000000000ull) __trap();
-          }
-          orb |= v & kBad;
-        }
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        if (need) {
-          for (int k = lane; k < G; k += 32) {
-            const unsigned long long d = *reinterpret_cast<volatile unsigned long long*>(dmx + k);
-            gm = d > gm ? d : gm;
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          orb |= __shfl_xor_sync(0xffffffffu, orb, o);
-          const unsigned long long x = __shfl_xor_sync(0xffffffffu, gm, o);
-          gm = x > gm ? x : gm;
-        }
-        if (lane == 0) {
-          s_seen = orb;
-          s_max[0] = gm;
-#ifdef RBF_TRACE
-          if (a.trace) {
-            unsigned long long* o = a.trace + ((step % a.trace_cap) * gridDim.x + blockIdx.x) * 4;
-            o[0] = tr0;
-            o[1] = tr1;
-            o[2] = globaltimer();
-            o[3] = static_cast<unsigned long long>(*reinterpret_cast<volatile long long*>(&s_issued) - (step + 1) * my_n);
-          }
-#endif
-        }
-      }
-    } else if (ctid == 0) {
+    if (ctid == 0) {
       unsigned int cbad = 0;
       unsigned long long cm = 0ull;
       for (int w = 1; w <= CW; ++w) {
@@ -596,8 +530,7 @@ stream_loop_kernel(StepArgs a, LoopArgs L, TmaGeom g) {
       bad_step = step;
       stop = true;
     } else if (need) {
-      const unsigned long long gm =
-          L.slots ? s_max[0] : *reinterpret_cast<volatile unsigned long long*>(&L.red[rs]);
+      const unsigned long long gm = *reinterpret_cast<volatile unsigned long long*>(&L.red[rs]);
       last_bits = gm;
       last_res_step = step;
       if (steady && __ddiv_rn(__longlong_as_double(static_cast<long long>(gm)), dt) <= tol) {
