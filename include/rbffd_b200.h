@@ -322,11 +322,20 @@ void rbf_group_destroy(rbf_group* group);
  *   rbf_group_push_import  all ranks' blobs, `stride` bytes apart; every rank
  *                          must import before any rank runs (hold a barrier)
  *   rbf_group_push_mode    1 when the group's fast path pushes
+ *   rbf_group_fused        1 when the last fixed-step fast run was ONE
+ *                          cooperative launch of the partitioned persistent
+ *                          loop: every local part's streaming loop on its own
+ *                          CTA range, the halo pushes fused into the lanes
+ *                          that compute the sent rows, a per-part grid
+ *                          barrier and release/acquire arrival counters
+ *                          between neighbours (RBFFD_PART_LOOP=0: the step +
+ *                          push kernels of the graph path instead)
  */
 int rbf_group_push_local(rbf_group* group);
 int rbf_group_push_export(rbf_group* group, void* blob_out, int64_t capacity, int64_t* length);
 int rbf_group_push_import(rbf_group* group, int32_t n_blobs, const void* blobs, int64_t stride);
 int rbf_group_push_mode(const rbf_group* group);
+int rbf_group_fused(const rbf_group* group);
 
 /* Host-paced push mode: after every fixed-mode step (and its halo pushes)
  * the group synchronises its stream and calls fn(ctx) -- a barrier across

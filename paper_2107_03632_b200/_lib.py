@@ -66,6 +66,7 @@ EXPORTED = (
     "rbf_group_push_export",
     "rbf_group_push_import",
     "rbf_group_push_mode",
+    "rbf_group_fused",
     "rbf_group_push_off",
     "rbf_error_norms",
     "rbf_host_alloc",
@@ -169,6 +170,7 @@ def load(path: os.PathLike | str | None = None) -> ctypes.CDLL:
         "rbf_group_push_export": ([vp, vp, i64, vp], i32),
         "rbf_group_push_import": ([vp, i32, vp, i64], i32),
         "rbf_group_push_mode": ([vp], i32),
+        "rbf_group_fused": ([vp], i32),
         "rbf_group_push_off": ([vp], i32),
         "rbf_error_norms": ([vp, vp, pdbl, pdbl], i32),
         "rbf_host_alloc": ([i64, ctypes.POINTER(vp)], i32),

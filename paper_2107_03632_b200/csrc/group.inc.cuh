@@ -94,6 +94,17 @@ struct rbf_group {
   // may not be running -- the cross-process path on ranks sharing one GPU
   void (*step_barrier)(void*) = nullptr;
   void* step_barrier_ctx = nullptr;
+  // partitioned persistent loop (part_loop_kernel): all local parts in one
+  // cooperative launch, halo pushes fused into the consumers
+  int part_loop_state = 0;               // 0 not prepared, 1 ready, -1 not applicable
+  PartLoopFn part_fn = nullptr;
+  size_t part_smem = 0;
+  int part_grid = 0, part_block = 0;
+  rbf::TmaGeom part_geom = {1, 2, 0, 0};
+  rbf::PartLoop* d_parts = nullptr;
+  std::vector<rbf::PartLoop> h_parts;
+  unsigned long long* d_bars = nullptr;  // [3] per part
+  std::vector<void*> part_bufs;          // push lists
 };
 
 // What one part publishes so that its peers can push into it (IPC mode).
@@ -303,6 +314,180 @@ int group_fast_graph(rbf_group* g, cudaGraphExec_t* out) {
   return RBF_OK;
 }
 
+void part_loop_release(rbf_group* g) {
+  for (void* b : g->part_bufs) cudaFree(b);
+  g->part_bufs.clear();
+  if (g->d_parts) cudaFree(g->d_parts);
+  if (g->d_bars) cudaFree(g->d_bars);
+  g->d_parts = nullptr;
+  g->d_bars = nullptr;
+  g->h_parts.clear();
+  g->part_loop_state = 0;
+}
+
+// Whether the fixed-step fast path can run as one part_loop_kernel launch
+// (push mode, every part on the persistent streaming loop with the same
+// kernel and ring geometry, identity numbering), and its descriptors.
+int part_loop_prepare(rbf_group* g) {
+  if (g->part_loop_state != 0) return RBF_OK;
+  g->part_loop_state = -1;
+  const char* env = std::getenv("RBFFD_PART_LOOP");
+  if ((env && std::atoi(env) == 0) || !g->push || g->step_barrier) return RBF_OK;
+  rbf_plan* p0 = g->parts[0];
+  for (rbf_plan* p : g->parts) {
+    if (!p->loop_fn || p->renumbered || p->n != p0->n || p->index_bits != p0->index_bits ||
+        p->loop_geom.sps != p0->loop_geom.sps || p->loop_geom.stages != p0->loop_geom.stages ||
+        p->loop_smem != p0->loop_smem || p->tma_block != p0->tma_block || p->N_i < 1)
+      return RBF_OK;
+  }
+  PartLoopFn fn = nullptr;
+  switch (p0->n) {
+#define RBF_PCASE(K) \
+  case K:            \
+    fn = KernelSet<K>::part_loop(p0->index_bits == 16); \
+    break;
+    RBF_SPECIALISED(RBF_PCASE)
+#undef RBF_PCASE
+    default:
+      return RBF_OK;
+  }
+  if (set_max_smem(fn) != cudaSuccess) {
+    cudaGetLastError();
+    return RBF_OK;
+  }
+  int sms = 0, occ = 0;
+  RBF_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, p0->tma_block, p0->loop_smem) != cudaSuccess ||
+      occ < 1) {
+    cudaGetLastError();
+    return RBF_OK;
+  }
+  const int total = sms * occ, np = static_cast<int>(g->parts.size());
+  if (np > total) return RBF_OK;
+  // CTAs per part in proportion to its slices (>= 1, <= its chunks)
+  const int sps = p0->loop_geom.sps;
+  int64_t S_all = 0;
+  for (rbf_plan* p : g->parts) S_all += p->S;
+  std::vector<int> ncta(np);
+  int used = 0;
+  for (int a = 0; a < np; ++a) {
+    const int64_t chunks = (g->parts[a]->S + sps - 1) / sps;
+    const int64_t want = std::max<int64_t>(1, (total - np) * g->parts[a]->S / std::max<int64_t>(S_all, 1) + 1);
+    ncta[a] = static_cast<int>(std::min<int64_t>(want, chunks));
+    used += ncta[a];
+  }
+  if (used > total) return RBF_OK;
+  g->h_parts.assign(np, rbf::PartLoop{});
+  int cta0 = 0;
+  for (int a = 0; a < np; ++a) {
+    rbf_plan* p = g->parts[a];
+    const rbf::PushArgs& pa = g->push_args[a];
+    rbf::PartLoop& P = g->h_parts[a];
+    const bool saved = p->push;
+    p->push = false;  // plain streaming args (the part loop waits by itself)
+    P.a = p->args();
+    p->push = saved;
+    P.U[0] = p->U[0];
+    P.U[1] = p->U[1];
+    P.cta0 = cta0;
+    P.ncta = ncta[a];
+    cta0 += ncta[a];
+    // per-slice push lists from the part's send segments
+    std::vector<int> cnt(static_cast<size_t>(p->S) + 1, 0);
+    std::vector<unsigned long long> ent;
+    int64_t first_push_row = p->N_i;
+    for (int i = 0; i < pa.n_peer; ++i) {
+      for (int64_t k = pa.peer[i].src_off; k < pa.peer[i].src_off + pa.peer[i].count; ++k) {
+        const int64_t row = static_cast<int64_t>(p->halo_send_idx_h[static_cast<size_t>(k)]) - p->B;
+        if (row < 0 || row >= p->N_i) return fail(RBF_ERR_PARAM, "send list entry outside the part's rows");
+        ++cnt[static_cast<size_t>(row >> 5) + 1];
+        first_push_row = std::min(first_push_row, row);
+      }
+    }
+    for (int64_t sl = 0; sl < p->S; ++sl) cnt[static_cast<size_t>(sl) + 1] += cnt[static_cast<size_t>(sl)];
+    if (cnt.back() > 0) {
+      if (static_cast<int64_t>(cnt.back()) >= (int64_t(1) << 31))
+        return RBF_OK;
+      ent.assign(static_cast<size_t>(cnt.back()), 0ull);
+      std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+      for (int i = 0; i < pa.n_peer; ++i) {
+        for (int64_t k = pa.peer[i].src_off; k < pa.peer[i].src_off + pa.peer[i].count; ++k) {
+          const int64_t row = static_cast<int64_t>(p->halo_send_idx_h[static_cast<size_t>(k)]) - p->B;
+          const unsigned long long slot =
+              static_cast<unsigned long long>(pa.peer[i].dst_off + (k - pa.peer[i].src_off));
+          if (slot >= (1ull << 52)) return RBF_OK;
+          ent[static_cast<size_t>(fill[static_cast<size_t>(row >> 5)]++)] =
+              (static_cast<unsigned long long>(i) << 58) | (static_cast<unsigned long long>(row & 31) << 52) | slot;
+        }
+      }
+      int* d_off = nullptr;
+      unsigned long long* d_ent = nullptr;
+      RBF_CK(cudaMalloc(&d_off, sizeof(int) * cnt.size()));
+      g->part_bufs.push_back(d_off);
+      RBF_CK(cudaMalloc(&d_ent, sizeof(unsigned long long) * ent.size()));
+      g->part_bufs.push_back(d_ent);
+      RBF_CK(cudaMemcpy(d_off, cnt.data(), sizeof(int) * cnt.size(), cudaMemcpyHostToDevice));
+      RBF_CK(cudaMemcpy(d_ent, ent.data(), sizeof(unsigned long long) * ent.size(), cudaMemcpyHostToDevice));
+      P.push_off = d_off;
+      P.push_ent = d_ent;
+    }
+    for (int i = 0; i < pa.n_peer; ++i) {
+      P.peer_u[i][0] = pa.peer[i].u[0];
+      P.peer_u[i][1] = pa.peer[i].u[1];
+    }
+    for (int j = 0; j < pa.n_nbr; ++j) P.nbr_flags[j] = pa.nbr_flags[j];
+    P.n_nbr = pa.n_nbr;
+    P.my_id = pa.my_id;
+    P.sys_scope = pa.sys_scope;
+    P.my_flags = p->push_flags;
+    P.wait_mask = 0;
+    for (int i = 0; i < p->wait_n; ++i) P.wait_mask |= 1ull << p->wait_ids[i];
+    P.sync_row0 = std::min<int64_t>(p->halo_row0, first_push_row);
+  }
+  RBF_CK(cudaMalloc(&g->d_bars, sizeof(unsigned long long) * 3 * np));
+  for (int a = 0; a < np; ++a) g->h_parts[a].bar = g->d_bars + 3 * a;
+  RBF_CK(cudaMalloc(&g->d_parts, sizeof(rbf::PartLoop) * np));
+  g->part_fn = fn;
+  g->part_smem = p0->loop_smem;
+  g->part_grid = cta0;
+  g->part_block = p0->tma_block;
+  g->part_geom = p0->loop_geom;
+  g->part_loop_state = 1;
+  return RBF_OK;
+}
+
+// Descriptors and barrier words of this run (before the timed region).
+int part_loop_upload(rbf_group* g) {
+  const int np = static_cast<int>(g->parts.size());
+  for (int a = 0; a < np; ++a) g->h_parts[a].base = static_cast<unsigned long long>(g->parts[a]->push_base);
+  RBF_CK(cudaMemcpyAsync(g->d_parts, g->h_parts.data(), sizeof(rbf::PartLoop) * np, cudaMemcpyHostToDevice,
+                         g->stream));
+  std::vector<unsigned long long> bars(static_cast<size_t>(3 * np), 0ull);
+  for (int a = 0; a < np; ++a) bars[static_cast<size_t>(3 * a + 1)] = ~0ull;
+  RBF_CK(cudaMemcpyAsync(g->d_bars, bars.data(), sizeof(unsigned long long) * bars.size(), cudaMemcpyHostToDevice,
+                         g->stream));
+  RBF_CK(cudaStreamSynchronize(g->stream));  // the host arrays above are pageable locals
+  return RBF_OK;
+}
+
+int part_loop_launch(rbf_group* g, int64_t limit) {
+  const int np = static_cast<int>(g->parts.size());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g->part_grid);
+  cfg.blockDim = dim3(g->part_block);
+  cfg.dynamicSmemBytes = g->part_smem;
+  cfg.stream = g->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // every part's CTAs co-resident
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const rbf::PartLoop* dp = g->d_parts;
+  RBF_CK(cudaLaunchKernelEx(&cfg, g->part_fn, dp, np, static_cast<long long>(limit), g->part_geom));
+  for (rbf_plan* p : g->parts) ++p->launches;
+  return RBF_OK;
+}
+
 // Fixed-mode run without per-step reductions.  On return *any_bad tells the
 // caller to restore the start field and replay on the exact per-step path.
 int group_run_fast(rbf_group* g, int64_t limit, bool* any_bad, unsigned long long* res_bits) {
@@ -313,18 +498,22 @@ int group_run_fast(rbf_group* g, int64_t limit, bool* any_bad, unsigned long lon
   }
   cudaGraphExec_t graph = nullptr;
   const bool paced = g->step_barrier != nullptr;
-  if (limit > kGroupGraph && !paced) RBF_TRY(group_fast_graph(g, &graph));
+  RBF_TRY(part_loop_prepare(g));
+  const bool fused = g->part_loop_state == 1;
+  if (limit > kGroupGraph && !paced && !fused) RBF_TRY(group_fast_graph(g, &graph));
   if (paced) {  // every rank finished its setup / previous run
     RBF_CK(cudaStreamSynchronize(g->stream));
     g->step_barrier(g->step_barrier_ctx);
   }
+  if (fused) RBF_TRY(part_loop_upload(g));
   RBF_CK(cudaEventRecord(g->ev0, g->stream));
-  const int64_t chunks = paced ? 0 : (limit - 1) / kGroupGraph;
+  if (fused) RBF_TRY(part_loop_launch(g, limit));
+  const int64_t chunks = (paced || fused) ? 0 : (limit - 1) / kGroupGraph;
   for (int64_t c = 0; c < chunks; ++c) {
     RBF_CK(cudaGraphLaunch(graph, g->stream));
     for (size_t a = 0; a < g->parts.size(); ++a) g->parts[a]->launches += g->graph_launches[a];
   }
-  for (int64_t s = chunks * kGroupGraph; s < limit; ++s) {
+  for (int64_t s = fused ? limit : chunks * kGroupGraph; s < limit; ++s) {
     RBF_TRY(group_fast_step(g, static_cast<int>(s & 1), s == limit - 1 ? rbf::kNeedResidual : 0));
     if (paced) {  // this step and its pushes are complete on every rank before any rank steps on
       RBF_CK(cudaStreamSynchronize(g->stream));
@@ -415,6 +604,8 @@ int rbf_plan_set_halo(rbf_plan* p, int32_t n_peers, const int32_t* peers, const 
   if (total > 0)
     RBF_CK(cudaMemcpyAsync(p->halo_send_idx, idx.data(), sizeof(int32_t) * total, cudaMemcpyHostToDevice,
                            p->stream));
+  RBF_CK(cudaStreamSynchronize(p->stream));
+  p->halo_send_idx_h = std::move(idx);
   // first row that reads a halo value: the TMA step overlaps the rows before
   // it with the neighbours' pushes (parts order their rows interior-first)
   int64_t h_lo = p->B, h_hi = 0;
@@ -615,6 +806,7 @@ int rbf_group_push_local(rbf_group* g) {
     cudaGraphExecDestroy(g->fast_graph);
     g->fast_graph = nullptr;
   }
+  part_loop_release(g);
   g->push = true;
   return RBF_OK;
 }
@@ -702,16 +894,19 @@ int rbf_group_push_import(rbf_group* g, int32_t n_blobs, const void* blobs, int6
     cudaGraphExecDestroy(g->fast_graph);
     g->fast_graph = nullptr;
   }
+  part_loop_release(g);
   g->push = true;
   return RBF_OK;
 }
 
 int rbf_group_push_mode(const rbf_group* g) { return g && g->push ? 1 : 0; }
+int rbf_group_fused(const rbf_group* g) { return g && g->part_loop_state == 1 ? 1 : 0; }
 
 int rbf_group_set_step_barrier(rbf_group* g, void (*fn)(void*), void* ctx) {
   if (!g) return fail(RBF_ERR_PARAM, "group is NULL");
   g->step_barrier = fn;
   g->step_barrier_ctx = ctx;
+  part_loop_release(g);
   return RBF_OK;
 }
 
@@ -725,6 +920,7 @@ int rbf_group_push_off(rbf_group* g) {
     cudaGraphExecDestroy(g->fast_graph);
     g->fast_graph = nullptr;
   }
+  part_loop_release(g);
   return RBF_OK;
 }
 
@@ -734,6 +930,7 @@ void rbf_group_destroy(rbf_group* g) {
   if (g->stream) cudaStreamSynchronize(g->stream);
   for (void* m : g->ipc_opened) cudaIpcCloseMemHandle(m);
   for (unsigned int* t : g->tickets) cudaFree(t);
+  part_loop_release(g);
   for (rbf_plan* p : g->parts) p->push = false;
   if (g->fast_graph) cudaGraphExecDestroy(g->fast_graph);
   if (g->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(g->comm);

@@ -82,6 +82,7 @@ using ResidentFn = void (*)(rbf::ResidentArgs);
 using ClusterFn = void (*)(rbf::ClusterArgs);
 using GridFn = void (*)(rbf::GridArgs);
 using LoopFn = void (*)(rbf::StepArgs, rbf::LoopArgs, rbf::TmaGeom);
+using PartLoopFn = void (*)(const rbf::PartLoop*, int, long long, rbf::TmaGeom);
 
 template <int NJ>
 struct KernelSet {
@@ -116,6 +117,15 @@ struct KernelSet {
   static LoopFn loop(bool idx16) {
     if constexpr (NJ > 0) {
       return idx16 ? rbf::stream_loop_kernel<NJ, kCW, 2> : rbf::stream_loop_kernel<NJ, kCW, 4>;
+    } else {
+      (void)idx16;
+      return nullptr;
+    }
+  }
+  // partitioned persistent loop of a push-mode group (group.inc.cuh)
+  static PartLoopFn part_loop(bool idx16) {
+    if constexpr (NJ > 0) {
+      return idx16 ? rbf::part_loop_kernel<NJ, kCW, 2> : rbf::part_loop_kernel<NJ, kCW, 4>;
     } else {
       (void)idx16;
       return nullptr;
@@ -267,6 +277,7 @@ struct rbf_plan {
   int wait_n = 0;
   int64_t push_base = 0;
   int* halo_send_idx = nullptr;     // [halo_send_total] local ids of owned nodes to send
+  std::vector<int32_t> halo_send_idx_h;  // host copy (the part loop's per-slice push lists)
   double* halo_sendbuf = nullptr;   // packed values, segments per peer
   int64_t halo_send_total = 0;
   int64_t halo_row0 = 0;            // first row that reads a halo node (rbf_plan_set_halo)

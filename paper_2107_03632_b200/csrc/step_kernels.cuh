@@ -564,6 +564,276 @@ stream_loop_kernel(StepArgs a, LoopArgs L, TmaGeom g) {
 }
 
 // ---------------------------------------------------------------------------
+// Partitioned persistent loop (fixed-step fast path of a
+// push-mode group): every local part of the group runs the streaming loop
+// above on its own CTA range of ONE cooperative launch, and the halo exchange
+// is fused into it.  A row whose value a neighbour part reads is stored
+// straight into the neighbour's field buffer (its halo slot in the buffer the
+// neighbour reads next step: P2P stores over NVLink when the neighbour is
+// another GPU's part mapped through CUDA IPC) by the consumer lane that
+// computed it.  Per step and part: part-local grid barrier (arrival counter);
+// its last arriver publishes "steps done" to every neighbour's arrival array
+// (release; system scope across GPUs).  A warp waits for its neighbours'
+// previous step before its first unit at or after `sync_row0` -- the first
+// row that reads a halo value or is pushed (parts order those rows last), so
+// interior rows overlap the neighbours' step -- and every CTA that pushes has
+// waited: no push overwrites a halo slot its neighbour still reads.
+// No early stop: the group's end-of-run reduction decides (first non-finite
+// step -> exact replay, solver.py:200-206), like the graph fast path.
+struct PartLoop {
+  StepArgs a;                 // W / C16 / C / meta / F / n_rows / dst_base / st of the part
+  double* U[2];               // the part's field buffers (start field in U[0])
+  int cta0, ncta;             // CTA range of the part in the launch
+  long long sync_row0;        // first row that reads a halo value or is pushed
+  unsigned long long* bar;    // [0] arrival counter, [1] first non-finite step (min), [2] residual bits (max)
+  const int* push_off;        // [S+1] per-slice ranges of push_ent (nullptr: no pushes)
+  const unsigned long long* push_ent;  // (peer << 58) | (lane << 52) | slot in the peer's numbering
+  double* peer_u[kMaxPushPeers][2];
+  unsigned long long* nbr_flags[kMaxPushPeers];  // neighbours' arrival arrays (this part writes [my_id])
+  const unsigned long long* my_flags;            // this part's arrival array (neighbours write [their id])
+  unsigned long long wait_mask;                  // neighbour ids to wait for
+  unsigned long long base;    // arrival count before this run (steps pushed in earlier runs)
+  int n_nbr, my_id, sys_scope;
+};
+
+__device__ __forceinline__ void wait_arrivals(const unsigned long long* flags, unsigned long long mask,
+                                              unsigned long long need) {
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned long long t0 = globaltimer();
+    for (unsigned long long m = mask; m; m &= m - 1) {
+      const int j = __ffsll(static_cast<long long>(m)) - 1;
+      while (ld_acquire_sys_u64(flags + j) < need) {
+        __nanosleep(32);
+        if (globaltimer() - t0 > 20000000000ull) __trap();
+      }
+    }
+  }
+  __syncwarp();
+}
+
+template <int NJ, int CW, int IB>
+__global__ void __launch_bounds__(32 * (CW + 1), 1)
+part_loop_kernel(const PartLoop* __restrict__ parts, int n_parts, long long limit, TmaGeom g) {
+  extern __shared__ __align__(128) unsigned char tma_smem[];
+  constexpr int kMaxStages = 16;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tma_smem);
+  uint64_t* empty = full + kMaxStages;
+  unsigned char* ring = tma_smem + 2 * kMaxStages * sizeof(uint64_t);
+  __shared__ long long s_issued;
+  __shared__ unsigned long long s_max[32];
+  __shared__ unsigned int s_bad[32];
+  int q_part = 0;
+  while (q_part + 1 < n_parts && static_cast<int>(blockIdx.x) >= parts[q_part + 1].cta0) ++q_part;
+  const PartLoop& P = parts[q_part];  // rarely used fields stay in global memory
+  const StepArgs a = P.a;
+  double* const U0 = P.U[0];
+  double* const U1 = P.U[1];
+  const long long sync_row0 = P.sync_row0;
+  const int* const push_off = P.push_off;
+  const unsigned long long* const push_ent = P.push_ent;
+  const unsigned long long* const my_flags = P.my_flags;
+  const unsigned long long wait_mask = P.wait_mask, fbase = P.base;
+  unsigned long long* const bar = P.bar;
+  const int sys_scope = P.sys_scope;
+  const int G = P.ncta, b = static_cast<int>(blockIdx.x) - P.cta0;
+  const int sps = g.sps, stages = g.stages;
+  const int wbytes = sps * NJ * 32 * 8, cbytes = sps * NJ * 32 * IB;
+  const int stage_bytes = sps * tma_slice_bytes<NJ, IB>();
+  const long long S = (a.n_rows + 31) >> 5;
+  const long long nchunks = (S + sps - 1) / sps;
+  const int my_n = b < nchunks ? static_cast<int>((nchunks - 1 - b) / G + 1) : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long total_q = limit * my_n;
+
+  if (threadIdx.x == 0) {
+    s_issued = 0;
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], static_cast<uint32_t>(sps));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {  // producer: the part's chunk sequence, step after step
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int i = 0, s = 0;
+      uint32_t ph = 1;
+      for (long long q = 0; q < total_q; ++q) {
+        if (q >= stages) mbar_wait(&empty[s], ph);
+        const long long c = b + static_cast<long long>(i) * G;
+        const long long s0 = c * sps;
+        const int ns = static_cast<int>(S - s0 < sps ? S - s0 : sps);
+        unsigned char* dst = ring + static_cast<size_t>(s) * stage_bytes;
+        const uint32_t wb = ns * NJ * 32 * 8, cb = ns * NJ * 32 * IB, fb = ns * 32 * 8;
+        const uint32_t mb = IB == 2 ? ns * 16 : 0;
+        mbar_expect_tx(&full[s], wb + cb + fb + mb);
+        bulk_g2s(dst, a.W + s0 * NJ * 32, wb, &full[s], pol);
+        if constexpr (IB == 2) {
+          bulk_g2s(dst + wbytes, a.C16 + s0 * NJ * 32, cb, &full[s], pol);
+          bulk_g2s(dst + wbytes + cbytes + sps * 32 * 8, a.meta + s0, mb, &full[s], pol);
+        } else {
+          bulk_g2s(dst + wbytes, a.C + s0 * NJ * 32, cb, &full[s], pol);
+        }
+        bulk_g2s(dst + wbytes + cbytes, a.F + s0 * 32, fb, &full[s], pol);
+        __threadfence_block();
+        *reinterpret_cast<volatile long long*>(&s_issued) = q + 1;
+        if (++i == my_n) i = 0;
+        if (++s == stages) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+      // every armed chunk is consumed before the consumers leave: no copy in flight
+    }
+    return;
+  }
+
+  // ---- consumer warps
+  const int ctid = threadIdx.x - 32, nthreads = 32 * CW;
+  const double dt = a.st->dt;
+  const int upc = sps;
+  for (long long step = 0; step < limit; ++step) {
+    const double* u_in = (step & 1) ? U1 : U0;
+    double* u_out = (step & 1) ? U0 : U1;
+    const int ob = static_cast<int>((step & 1) ^ 1);  // the neighbours' buffer this step writes
+    const bool need = step == limit - 1;
+    bool bad = false, waited = wait_mask == 0ull;
+    unsigned long long dmax = 0ull;
+    const long long qbase = step * my_n;
+    const long long qdiv = qbase / stages;
+    const int qmod = static_cast<int>(qbase - qdiv * stages);
+    const uint32_t qpar = static_cast<uint32_t>(qdiv & 1);
+    for (int uq = warp - 1; uq < my_n * upc; uq += CW) {
+      const int i = uq / upc, slot = uq - i * upc;
+      const long long q = qbase + i;
+      const int t = qmod + i, tdiv = t / stages;
+      const int s = t - tdiv * stages;
+      const uint32_t ph = (qpar + static_cast<uint32_t>(tdiv)) & 1u;
+      if (lane == 0) {
+        while (*reinterpret_cast<volatile long long*>(&s_issued) <= q) __nanosleep(64);
+      }
+      __syncwarp();
+      mbar_wait(&full[s], ph);
+      const unsigned char* base = ring + static_cast<size_t>(s) * stage_bytes;
+      const long long slice = (b + static_cast<long long>(i) * G) * sps + slot;
+      if (!waited && (slice + 1) * 32 > sync_row0) {
+        wait_arrivals(my_flags, wait_mask, fbase + static_cast<unsigned long long>(step));
+        waited = true;
+      }
+      const long long r = slice * 32 + lane;
+      double value = 0.0;
+      if (slice < S && r < a.n_rows) {
+        double gv[NJ];
+        int c0;
+        if constexpr (IB == 2) {
+          const int4 m = reinterpret_cast<const int4*>(base + wbytes + cbytes + sps * 32 * 8)[slot];
+          if (m.z) {
+            const unsigned short* sC = reinterpret_cast<const unsigned short*>(base + wbytes) + slot * NJ * 32;
+            c0 = decode_id(sC[lane], m);
+            gv[0] = ld_field(u_in + c0);
+#pragma unroll
+            for (int j = 1; j < NJ; ++j) gv[j] = ld_field(u_in + decode_id(sC[j * 32 + lane], m));
+          } else {
+            const int* gC = a.C + slice * NJ * 32 + lane;
+            c0 = __ldg(gC);
+            gv[0] = ld_field(u_in + c0);
+#pragma unroll
+            for (int j = 1; j < NJ; ++j) gv[j] = ld_field(u_in + __ldg(gC + 32 * j));
+          }
+        } else {
+          const int* sC = reinterpret_cast<const int*>(base + wbytes) + slot * NJ * 32;
+          c0 = sC[lane];
+          gv[0] = ld_field(u_in + c0);
+#pragma unroll
+          for (int j = 1; j < NJ; ++j) gv[j] = ld_field(u_in + sC[j * 32 + lane]);
+        }
+        const long long node = a.dst_base + r;
+        const double u_self = (c0 == node) ? gv[0] : ld_field(u_in + node);
+        const double* sW = reinterpret_cast<const double*>(base) + slot * NJ * 32;
+        const double* sF = reinterpret_cast<const double*>(base + wbytes + cbytes) + slot * 32;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc = __dadd_rn(acc, __dmul_rn(sW[j * 32 + lane], gv[j]));
+        value = __dadd_rn(u_self, __dmul_rn(dt, __dadd_rn(sF[lane], acc)));
+        u_out[node] = value;
+        if (!isfinite(value)) bad = true;
+        if (need) {
+          const unsigned long long bb =
+              static_cast<unsigned long long>(__double_as_longlong(fabs(__dsub_rn(value, u_self))));
+          dmax = bb > dmax ? bb : dmax;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      // fused halo push: this slice's rows the neighbours read, straight into
+      // their next-step buffer (warp-uniform range; the matching lane stores)
+      if (push_off && slice < S) {
+        const int pb = __ldg(push_off + slice), pe = __ldg(push_off + slice + 1);
+        for (int k = pb; k < pe; ++k) {
+          const unsigned long long e = __ldg(push_ent + k);
+          if (static_cast<int>((e >> 52) & 31) == lane)
+            P.peer_u[e >> 58][ob][e & ((1ull << 52) - 1)] = value;
+        }
+      }
+    }
+    // (a warp that neither read a halo value nor pushed need not wait: the
+    // part's arrival below certifies its own reads and pushes of this step)
+    const unsigned int wb = __ballot_sync(0xffffffffu, bad) ? 1u : 0u;
+    const unsigned long long wm = need ? warp_max_u64(dmax) : 0ull;
+    if (lane == 0) {
+      s_bad[warp] = wb;
+      s_max[warp] = wm;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+    if (ctid == 0) {
+      unsigned int cbad = 0;
+      unsigned long long cm = 0ull;
+      for (int w = 1; w <= CW; ++w) {
+        cbad |= s_bad[w];
+        cm = s_max[w] > cm ? s_max[w] : cm;
+      }
+      if (cbad) atomicMin(&bar[1], static_cast<unsigned long long>(step));
+      if (need && cm) atomicMax(&bar[2], cm);
+      if (sys_scope) __threadfence_system();  // field stores and P2P pushes before the arrival
+      else __threadfence();
+      const unsigned long long target = static_cast<unsigned long long>(step + 1) * G;
+      const unsigned long long old = atomicAdd(&bar[0], 1ull);
+      if (old == target - 1) {  // last arriver of the part: tell the neighbours
+        const unsigned long long v = fbase + static_cast<unsigned long long>(step + 1);
+        if (sys_scope) __threadfence_system();
+        else __threadfence();
+        for (int j = 0; j < P.n_nbr; ++j) {
+          if (sys_scope)
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.nbr_flags[j] + P.my_id), "l"(v) : "memory");
+          else
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(P.nbr_flags[j] + P.my_id), "l"(v) : "memory");
+        }
+      } else {
+        unsigned long long v;
+        const unsigned long long t0 = globaltimer();
+        for (int spin = 0;; ++spin) {
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&bar[0]) : "memory");
+          if (v >= target) break;
+          if ((spin & 1023) == 1023 && globaltimer() - t0 > 20000000000ull) __trap();
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+  }
+  if (b == 0 && ctid == 0) {  // the last barrier: every CTA of the part is done
+    DevStatus* st = a.st;
+    const unsigned long long fb = *reinterpret_cast<volatile unsigned long long*>(&bar[1]);
+    st->bad_step = fb == ~0ull ? -1 : static_cast<long long>(fb);
+    st->conv_step = -1;
+    st->last_res_bits = *reinterpret_cast<volatile unsigned long long*>(&bar[2]);
+    st->last_res_step = limit - 1;
+    st->step = limit;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Resident loop: the whole problem (weights, ids, forcing, both field buffers)
 // lives in one CTA's shared memory and the CTA runs every step of the loop
 // on-chip.  Used when the working set fits (the paper's Fig. 1 case, N=1025,

@@ -118,7 +118,9 @@ class RankSetup:
         if reads_halo.any():
             order = np.argsort(reads_halo, kind="stable")
             rows_ref, own_nodes_h, rows_g = rows_ref[order], own_nodes_h[order], rows_g[order]
+            reads_halo = reads_halo[order]
             own_nodes = torch.from_numpy(own_nodes_h).to(dev)
+        self._reads_halo = reads_halo  # finish() moves the rows peers read before these
         self.rows_ref = rows_ref
         # final row position of the own nodes (slot keeps the Morton position
         # of every interior node: it orders the halo groups on every rank)
@@ -179,13 +181,43 @@ class RankSetup:
                 self.recv[q] = (B + int(s0), int(e0 - s0))
                 self.requests[q] = halo_h[s0:e0].astype(np.int64)  # global ids, in this rank's halo order
 
-    def finish(self, requests_by_rank) -> Part:
-        """requests_by_rank[p] = rank p's ``requests`` dict (all ranks)."""
-        base = self.B + self.H
+    def _rows_of(self, ids):  # row positions of own global node ids
         own_sorted = self._own_nodes[self._own_sorted]
+        return self._own_sorted[np.searchsorted(own_sorted, ids)]
 
-        def rows_of(ids):  # final row positions of own global node ids
-            return self._own_sorted[np.searchsorted(own_sorted, ids)]
+    def finish(self, requests_by_rank) -> Part:
+        """requests_by_rank[p] = rank p's ``requests`` dict (all ranks).
+
+        Rows are put in multigpu.partition's three groups: rows no other rank
+        reads and that read no halo value, rows only read by other ranks, rows
+        that read a halo value (each in Morton order)."""
+        base = self.B + self.H
+        sent = np.zeros(self.n_own, dtype=bool)
+        for p, req in enumerate(requests_by_rank):
+            if p != self.rank and self.rank in req:
+                sent[self._rows_of(req[self.rank])] = True
+        group = np.where(self._reads_halo, 2, np.where(sent, 1, 0))
+        perm = np.argsort(group, kind="stable")
+        if not np.array_equal(perm, np.arange(self.n_own)):
+            inv = np.empty_like(perm)
+            inv[perm] = np.arange(perm.size)
+            self.rows_ref = self.rows_ref[perm]
+            self._own_nodes = self._own_nodes[perm]
+            self._own_sorted = np.argsort(self._own_nodes, kind="stable")
+            self.f_int = np.ascontiguousarray(self.f_int[perm])
+            rows = self.rows[perm]
+            flat = rows.reshape(-1)
+            for lo in range(0, flat.size, _CHUNK):
+                seg = flat[lo:lo + _CHUNK]
+                m = seg >= base
+                seg[m] = base + inv[seg[m] - base]
+            self.rows = rows
+            self.l2g = self.l2g.copy()
+            self.l2g[base:] = self._own_nodes
+            self.positions_local = np.ascontiguousarray(self.positions_local)
+            self.positions_local[base:] = self.positions_local[base:][perm]
+            self._reads_halo = self._reads_halo[perm]
+        rows_of = self._rows_of
 
         send_to = {p: rows_of(req[self.rank]) for p, req in enumerate(requests_by_rank)
                    if p != self.rank and self.rank in req}

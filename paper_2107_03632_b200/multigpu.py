@@ -124,16 +124,26 @@ def partition(n_total: int, interior: np.ndarray, rows: np.ndarray, weights: np.
         ks = perm[bounds[p]:bounds[p + 1]]
         owner[interior[ks]] = p
         mslot[interior[ks]] = np.arange(ks.size)
-    # each part's rows interior-first: rows that read no halo value (only own
-    # and Dirichlet nodes) before the rest, each group in Morton order, so the
-    # push-mode step overlaps them with the exchange (StepArgs::halo_row0)
+    # each part's rows interior-first, in three groups, each in Morton order:
+    # rows that neither read a halo value nor are read by another part, then
+    # rows only read by another part (pushed), then rows that read a halo
+    # value -- the push-mode step overlaps the first group with the exchange
+    # (StepArgs::halo_row0, PartLoop::sync_row0)
+    sent = np.zeros(n_total, dtype=bool)  # interior nodes some other part's rows read
+    row_owner = owner[interior]
+    for lo in range(0, n_rows, 1 << 20):
+        r = rows[lo:lo + (1 << 20)]
+        of = owner[r]
+        cross = (of >= 0) & (of != row_owner[lo:lo + (1 << 20), None])
+        sent[r[cross]] = True
     own_ks = []
     slot = np.full(n_total, -1, dtype=np.int64)  # final row position of a node in its owner
     for p in range(n_parts):
         ks = perm[bounds[p]:bounds[p + 1]]
         of = owner[rows[ks]]
         reads_halo = ((of >= 0) & (of != p)).any(axis=1)
-        ks = ks[np.argsort(reads_halo, kind="stable")]
+        group = np.where(reads_halo, 2, np.where(sent[interior[ks]], 1, 0))
+        ks = ks[np.argsort(group, kind="stable")]
         own_ks.append(ks)
         slot[interior[ks]] = np.arange(ks.size)
 
@@ -239,6 +249,12 @@ class _Group:
     def push_mode(self) -> bool:
         """True when the fixed-step fast path pushes halos peer-to-peer."""
         return bool(self._lib.rbf_group_push_mode(self._h))
+
+    @property
+    def fused(self) -> bool:
+        """True when the last fixed-step fast run was one launch of the
+        partitioned persistent loop (halo pushes fused into the step)."""
+        return bool(self._lib.rbf_group_fused(self._h))
 
     def _push_local(self):
         self.plans[0]._check(self._lib.rbf_group_push_local(self._h))

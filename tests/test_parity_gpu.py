@@ -738,15 +738,18 @@ def test_partitioned_group_instability_and_synthetic(golden, synth_cache):
     group.close()
 
 
-@pytest.mark.parametrize("push", [True, False], ids=["p2p-push", "copy-exchange"])
+@pytest.mark.parametrize("push,fused", [(True, True), (True, False), (False, False)],
+                         ids=["fused-part-loop", "p2p-push-kernels", "copy-exchange"])
 @pytest.mark.parametrize("P", [2, 5])
-def test_partitioned_push_mode_runs(synth_cache, push, P):
-    """Push-mode halos (push_halo_kernel stores into the peers' buffers and
-    signals arrivals; the next step waits on them) against the copy exchange
-    and the oracle, over repeated runs (the arrival counters keep counting
-    across runs), odd step counts and graph-chunked runs."""
+def test_partitioned_push_mode_runs(synth_cache, monkeypatch, push, fused, P):
+    """Push-mode halos against the copy exchange and the oracle, over
+    repeated runs (the arrival counters keep counting across runs), odd step
+    counts and graph-chunked runs: the fused partitioned persistent loop (all
+    parts in one launch, pushes from the lanes that compute the sent rows)
+    and the step + push_halo_kernel graph path."""
     from paper_2107_03632_b200.multigpu import LocalGroup, partition, run_partitioned
 
+    monkeypatch.setenv("RBFFD_PART_LOOP", "1" if fused else "0")
     nodes, _, shapes = _synth(synth_cache, 200_000, 15, 2)
     interior = shapes.interior_nodes
     parts = partition(nodes.n_total, interior, shapes.stencils.neighbors[interior], shapes.weights,
@@ -759,6 +762,7 @@ def test_partitioned_push_mode_runs(synth_cache, push, P):
         want = orc.run_time_loop(nodes, shapes, steps=steps)
         assert done == steps and residual == want["residual"], steps
         assert np.array_equal(field, want["field"]), steps
+        assert group.fused == fused, steps
     # a failure inside a pushed run replays on the exact path (same step as the oracle)
     cfg = rb.SolveConfig(degree=2, support_size=15, nodes=200_000, steps=300, dt=40.0 * rb.stability_bound(shapes))
     want = orc.run_time_loop(nodes, shapes, dt=cfg.dt, steps=300)

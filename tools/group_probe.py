@@ -3,6 +3,7 @@
 All parts run in order on one device, so a P-part step costs the sum of the
 parts' steps plus the exchange: compare against one plan over all rows.
 """
+import os
 import sys
 import time
 
@@ -34,7 +35,8 @@ for persist in (False, True):
     del plan
 for P in (2, 4):
     parts = partition(nodes.n_total, interior, rows, sh.weights, f, nodes.positions, P)
-    for push in (True, False):
+    for label, push, fused in (("fused part loop", True, "1"), ("push kernels", True, "0"), ("copy", False, "0")):
+        os.environ["RBFFD_PART_LOOP"] = fused
         g = LocalGroup(parts, push=push)
         for part, p in zip(parts, g.plans):
             p.set_field(part.local_field(u0))
@@ -46,6 +48,6 @@ for P in (2, 4):
             rc, done, res, bad, sec = g.run(dt, steps=steps)
             best = min(best, sec / steps)
         halo = sum(pt.halo_bytes_per_step() for pt in parts)
-        print(f"  P={P} {'push' if push else 'copy'}: {1e6 * best:.2f} us/step for all parts "
+        print(f"  P={P} {label} (fused={g.fused}): {1e6 * best:.2f} us/step for all parts "
               f"(+{1e6 * (best - t1):.2f} us vs one plan; halo {halo / 1e3:.0f} kB/step)", flush=True)
         g.close()
