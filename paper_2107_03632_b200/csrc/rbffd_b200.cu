@@ -236,8 +236,6 @@ struct rbf_plan {
   int loop_grid = 0;
   rbf::TmaGeom loop_geom = {1, 2, 0, 0};
   unsigned long long* loop_red = nullptr;  // [7] residual slots + arrival counter
-  unsigned char* loop_packed = nullptr;    // chunk-contiguous stream of the loop (RBFFD_LOOP_PACKED)
-  bool loop_packed_dirty = true;           // re-pack before the next loop run (forcing changed)
   int grid_ctas = 0, grid_spc = 0, grid_spr = 0;
   size_t grid_smem = 0;
   unsigned long long* grid_red = nullptr;  // [3][2] per-step partial slots
@@ -862,18 +860,7 @@ int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
 // the final field is published into both buffers.
 int run_loop(rbf_plan* p, int64_t limit, bool steady) {
   RBF_CK(cudaMemsetAsync(p->loop_red, 0, 7 * sizeof(unsigned long long), p->stream));
-  if (p->loop_packed && p->loop_packed_dirty) {
-    const int blocks = static_cast<int>(std::min<int64_t>((p->S * 32 + 255) / 256, 148 * 16));
-    rbf::pack_chunks_kernel<<<blocks, 256, 0, p->stream>>>(
-        p->W, p->index_bits == 16 ? static_cast<const void*>(p->C16) : static_cast<const void*>(p->C), p->meta,
-        p->F, p->S, p->n, p->loop_geom.sps, p->index_bits / 8,
-        p->loop_geom.sps * (p->n * 32 * (8 + p->index_bits / 8) + 32 * 8 + (p->index_bits == 16 ? 16 : 0)),
-        p->loop_packed);
-    RBF_CK(cudaGetLastError());
-    p->loop_packed_dirty = false;
-  }
   rbf::LoopArgs L;
-  L.packed = p->loop_packed;
   L.U0 = p->U[0];
   L.U1 = p->U[1];
   L.limit = limit;
@@ -1237,16 +1224,6 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
         int lres = 0;
         if (const char* e = std::getenv("RBFFD_LOOP_RES")) lres = std::max(0, std::atoi(e));
         p->loop_geom = rbf::TmaGeom{lsps, stages, 0, lres};
-        // chunk-contiguous copy of the stream (one bulk copy per chunk), when
-        // requested and the copy fits in a quarter of the free memory
-        if (const char* e = std::getenv("RBFFD_LOOP_PACKED")) {
-          const size_t pbytes = static_cast<size_t>((p->S + lsps - 1) / lsps) * stage;
-          size_t free_b = 0, total_b = 0;
-          if (std::atoi(e) == 1 && cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && pbytes <= free_b / 4) {
-            RBF_TRY(dev_alloc(p.get(), &p->loop_packed, pbytes));
-            p->loop_packed_dirty = true;
-          }
-        }
       }
     }
     cudaGetLastError();
@@ -2016,7 +1993,6 @@ int rbf_set_forcing(rbf_plan* p, const double* f_int) {
     rbf::scatter_rows_kernel<<<blocks, 256, 0, p->stream>>>(p->tmp, p->row_of_k, p->N_i, p->F);
     RBF_CK(cudaGetLastError());
   }
-  p->loop_packed_dirty = true;  // the loop's packed stream carries F
   // the two-step tables carry a copy of the halo rows' forcing
   if (p->pair_ok) RBF_TRY(rbf::pair_refresh_forcing(&p->pair, p->stream));
   if (p->grid_two) RBF_TRY(rbf::pair_refresh_forcing(&p->grid_pair, p->stream));
@@ -2351,7 +2327,6 @@ void rbf_plan_destroy(rbf_plan* p) {
   pool_free(p->cluster_dest, s);
   pool_free(p->grid_red, s);
   pool_free(p->loop_red, s);
-  pool_free(p->loop_packed, s);
   pool_free(p->C16, s);
   pool_free(p->meta, s);
   pool_free(p->u_init, s);

@@ -302,38 +302,7 @@ struct LoopArgs {
   long long limit;             // steps to run (fixed: steps, steady: max_steps)
   int flags;                   // kSteady
   unsigned long long* red;     // [0..2] residual slots, [6] arrival counter
-  // non-null: the stream packed chunk-contiguously in the ring's stage
-  // layout (pack_chunks_kernel): one bulk copy per chunk instead of four
-  const unsigned char* packed;
 };
-
-// Chunk-contiguous copy of the streamed arrays for the persistent loop: chunk
-// c (sps slices) occupies [c * stage_bytes, (c+1) * stage_bytes) laid out as
-// the ring stage (W | ids | F | window bases), so the producer moves it with
-// one bulk copy (fewer, larger DRAM requests than four separate streams).
-__global__ void pack_chunks_kernel(const double* __restrict__ W, const void* __restrict__ ids,
-                                   const int4* __restrict__ meta, const double* __restrict__ F, long long S,
-                                   int n, int sps, int ib, int stage_bytes, unsigned char* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const long long wbytes = static_cast<long long>(sps) * n * 32 * 8, cbytes = static_cast<long long>(sps) * n * 32 * ib;
-  for (long long sl = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; sl < S;
-       sl += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
-    const long long c = sl / sps;
-    const int t = static_cast<int>(sl - c * sps);
-    unsigned char* base = out + c * stage_bytes;
-    const int4* w = reinterpret_cast<const int4*>(W + sl * n * 32);
-    int4* wd = reinterpret_cast<int4*>(base + static_cast<long long>(t) * n * 32 * 8);
-    for (int k = lane; k < n * 16; k += 32) wd[k] = w[k];
-    const int4* cs = reinterpret_cast<const int4*>(static_cast<const unsigned char*>(ids) + sl * n * 32 * ib);
-    int4* cd = reinterpret_cast<int4*>(base + wbytes + static_cast<long long>(t) * n * 32 * ib);
-    for (int k = lane; k < n * 2 * ib; k += 32) cd[k] = cs[k];
-    const int4* fs = reinterpret_cast<const int4*>(F + sl * 32);
-    int4* fd = reinterpret_cast<int4*>(base + wbytes + cbytes + t * 256);
-    if (lane < 16) fd[lane] = fs[lane];
-    if (ib == 2 && lane == 0)
-      reinterpret_cast<int4*>(base + wbytes + cbytes + sps * 256)[t] = meta[sl];
-  }
-}
 
 template <int NJ, int CW, int IB>
 __global__ void __launch_bounds__(32 * (CW + 1), 1)
@@ -403,20 +372,15 @@ stream_loop_kernel(StepArgs a, LoopArgs L, TmaGeom g) {
         const uint32_t wb = ns * NJ * 32 * 8, cb = ns * NJ * 32 * IB, fb = ns * 32 * 8;
         const uint32_t mb = IB == 2 ? ns * 16 : 0;
         const uint64_t pol = i < g.res ? pol_last : pol_first;
-        if (L.packed) {
-          mbar_expect_tx(&full[s], static_cast<uint32_t>(stage_bytes));
-          bulk_g2s(dst, L.packed + c * stage_bytes, static_cast<uint32_t>(stage_bytes), &full[s], pol);
+        mbar_expect_tx(&full[s], wb + cb + fb + mb);
+        bulk_g2s(dst, a.W + s0 * NJ * 32, wb, &full[s], pol);
+        if constexpr (IB == 2) {
+          bulk_g2s(dst + wbytes, a.C16 + s0 * NJ * 32, cb, &full[s], pol);
+          bulk_g2s(dst + wbytes + cbytes + sps * 32 * 8, a.meta + s0, mb, &full[s], pol);
         } else {
-          mbar_expect_tx(&full[s], wb + cb + fb + mb);
-          bulk_g2s(dst, a.W + s0 * NJ * 32, wb, &full[s], pol);
-          if constexpr (IB == 2) {
-            bulk_g2s(dst + wbytes, a.C16 + s0 * NJ * 32, cb, &full[s], pol);
-            bulk_g2s(dst + wbytes + cbytes + sps * 32 * 8, a.meta + s0, mb, &full[s], pol);
-          } else {
-            bulk_g2s(dst + wbytes, a.C + s0 * NJ * 32, cb, &full[s], pol);
-          }
-          bulk_g2s(dst + wbytes + cbytes, a.F + s0 * 32, fb, &full[s], pol);
+          bulk_g2s(dst + wbytes, a.C + s0 * NJ * 32, cb, &full[s], pol);
         }
+        bulk_g2s(dst + wbytes + cbytes, a.F + s0 * 32, fb, &full[s], pol);
         __threadfence_block();
         *reinterpret_cast<volatile long long*>(&s_issued) = q + 1;
         if (++i == my_n) i = 0;
