@@ -143,6 +143,7 @@ enum StepFlags : int {
   kSteady = 2,        // compare residual with tol and set conv_step
   kDistributed = 4,   // partitioned run: only accumulate red[]; the group's
                       // all-reduce + decide_kernel finalise the step
+  kPublish = 8,       // persistent loop: copy the final field into both buffers
 };
 
 

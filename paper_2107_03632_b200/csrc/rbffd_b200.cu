@@ -857,14 +857,14 @@ int run_resident(rbf_plan* p, int64_t limit, bool steady, bool copy_back) {
 }
 
 // The whole run in one cooperative launch of the persistent streaming loop;
-// the final field is published into both buffers.
-int run_loop(rbf_plan* p, int64_t limit, bool steady) {
+// with kPublish (copy-back runs) the final field is published into both buffers.
+int run_loop(rbf_plan* p, int64_t limit, bool steady, bool publish) {
   RBF_CK(cudaMemsetAsync(p->loop_red, 0, 7 * sizeof(unsigned long long), p->stream));
   rbf::LoopArgs L;
   L.U0 = p->U[0];
   L.U1 = p->U[1];
   L.limit = limit;
-  L.flags = steady ? rbf::kSteady : 0;
+  L.flags = (steady ? rbf::kSteady : 0) | (publish ? rbf::kPublish : 0);
   L.red = p->loop_red;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p->loop_grid);
@@ -2132,8 +2132,8 @@ int rbf_run(rbf_plan* p, double dt, int64_t steps, int32_t mode, double tol, int
   if (p->resident) {
     rc = run_resident(p, limit, steady, copy_back != 0);
   } else if (p->loop_fn && limit >= 1 && !(p->pair_forced && !steady && limit >= 2)) {
-    rc = run_loop(p, limit, steady);
-    published = true;
+    rc = run_loop(p, limit, steady, copy_back != 0);
+    published = copy_back != 0;  // else the final field is in U[st.step & 1]
     looped = true;
   } else if (p->pair_ok && !steady && limit >= 2) {
     bool fallback = false;

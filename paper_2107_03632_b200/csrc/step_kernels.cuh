@@ -544,11 +544,12 @@ stream_loop_kernel(StepArgs a, LoopArgs L, TmaGeom g) {
     }
   }
   if (ctid == 0) *reinterpret_cast<volatile int*>(&s_stop) = 1;  // release the producer
-  // publish the final field (buffer step & 1) into the other buffer too:
-  // every CTA copies the rows it wrote
+  // with kPublish (copy-back runs): the final field (buffer step & 1) into
+  // the other buffer too, every CTA copying the rows it wrote; otherwise the
+  // host takes buffer st->step & 1 as the current one
   const double* uf = (step & 1) ? L.U1 : L.U0;
   double* uo = (step & 1) ? L.U0 : L.U1;
-  for (int uq = warp - 1; uq < my_n * upc; uq += CW) {
+  for (int uq = warp - 1; (L.flags & kPublish) && uq < my_n * upc; uq += CW) {
     const int i = uq / upc, slot = uq - i * upc;
     const long long slice = (blockIdx.x + static_cast<long long>(i) * gridDim.x) * sps + slot;
     const long long r = slice * 32 + lane;
