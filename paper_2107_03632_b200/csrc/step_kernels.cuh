@@ -770,7 +770,7 @@ part_loop_kernel(const PartLoop* __restrict__ parts, int n_parts, long long limi
       if (lane == 0) mbar_arrive(&empty[s]);
       // fused halo push: this slice's rows the neighbours read, straight into
       // their next-step buffer (warp-uniform range; the matching lane stores)
-      if (push_off && slice < S) {
+      if (push_off && slice < S && (slice + 1) * 32 > sync_row0) {  // no sent row before sync_row0
         const int pb = __ldg(push_off + slice), pe = __ldg(push_off + slice + 1);
         for (int k = pb; k < pe; ++k) {
           const unsigned long long e = __ldg(push_ent + k);

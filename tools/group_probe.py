@@ -33,7 +33,7 @@ for persist in (False, True):
     if not persist:
         t1 = t  # the parts run the graph loop: compare like with like
     del plan
-for P in (2, 4):
+for P in (1, 2, 4):
     parts = partition(nodes.n_total, interior, rows, sh.weights, f, nodes.positions, P)
     for label, push, fused in (("fused part loop", True, "1"), ("push kernels", True, "0"), ("copy", False, "0")):
         os.environ["RBFFD_PART_LOOP"] = fused
