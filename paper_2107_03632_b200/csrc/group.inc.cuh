@@ -506,6 +506,13 @@ int group_run_fast(rbf_group* g, int64_t limit, bool* any_bad, unsigned long lon
     g->step_barrier(g->step_barrier_ctx);
   }
   if (fused) RBF_TRY(part_loop_upload(g));
+  if (!g->d_red) RBF_CK(cudaMalloc(&g->d_red, 2 * sizeof(long long)));
+  if (g->nccl && g->push) {
+    // every rank has set its start field (rbf_set_field is synchronous)
+    // before any rank's first push can land in its buffers: a one-element
+    // all-reduce orders this launch after every rank's call
+    RBF_NCK(g_nccl.AllReduce(g->d_red, g->d_red, 1, ncclInt64, ncclMax, g->comm, g->stream));
+  }
   RBF_CK(cudaEventRecord(g->ev0, g->stream));
   if (fused) RBF_TRY(part_loop_launch(g, limit));
   const int64_t chunks = (paced || fused) ? 0 : (limit - 1) / kGroupGraph;
@@ -525,7 +532,6 @@ int group_run_fast(rbf_group* g, int64_t limit, bool* any_bad, unsigned long lon
     if (g->push) p->push_base += limit;  // every part ran all `limit` pushes
   }
   // end-of-run reduction over all parts: min first-bad-step, max residual bits
-  if (!g->d_red) RBF_CK(cudaMalloc(&g->d_red, 2 * sizeof(long long)));
   long long key = std::numeric_limits<long long>::max();
   unsigned long long bits = 0;
   RBF_CK(cudaStreamSynchronize(g->stream));
