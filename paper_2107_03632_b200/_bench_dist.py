@@ -139,9 +139,15 @@ def main(args, metric, workloads):  # pragma: no cover - needs >1 GPU (or --forc
             "config": {"workload": (f"{desc}, split over {world} GPUs (strong scaling)" if strong else
                                     f"{desc} per GPU (weak scaling: one disk of {N} nodes)"),
                        "N": N, "N_i": n_rows_total, "n": n, "m": m, "dt": dt,
-                       "parallelism": (f"node-partitioned x{world}, halo exchange: "
-                                       + ("P2P push over NVLink (CUDA IPC), fused arrival flags"
-                                          if group.push_mode else "NCCL send/recv")),
+                       "parallelism": (f"node-partitioned x{world}, "
+                                       + ("fused partitioned persistent loop (one launch per run; halo "
+                                          "values pushed P2P over NVLink through CUDA IPC by the lanes "
+                                          "that compute them, release/acquire arrival counters)"
+                                          if group.fused and group.push_mode else
+                                          "fused partitioned persistent loop (one part: no exchange)"
+                                          if group.fused else
+                                          "halo exchange: P2P push kernels over NVLink (CUDA IPC)"
+                                          if group.push_mode else "halo exchange: NCCL send/recv")),
                        "halo_bytes_per_step_max_rank": int(halo.item()),
                        "setup_seconds": t_setup, "node_generation_seconds": t_nodes},
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s per GPU",

@@ -332,7 +332,10 @@ int part_loop_prepare(rbf_group* g) {
   if (g->part_loop_state != 0) return RBF_OK;
   g->part_loop_state = -1;
   const char* env = std::getenv("RBFFD_PART_LOOP");
-  if ((env && std::atoi(env) == 0) || !g->push || g->step_barrier) return RBF_OK;
+  if ((env && std::atoi(env) == 0) || g->step_barrier) return RBF_OK;
+  bool any_peer = false;  // without push mode, only parts that exchange nothing
+  for (rbf_plan* p : g->parts) any_peer = any_peer || !p->halo_peers.empty();
+  if (!g->push && any_peer) return RBF_OK;
   rbf_plan* p0 = g->parts[0];
   for (rbf_plan* p : g->parts) {
     if (!p->loop_fn || p->renumbered || p->n != p0->n || p->index_bits != p0->index_bits ||
@@ -381,7 +384,7 @@ int part_loop_prepare(rbf_group* g) {
   int cta0 = 0;
   for (int a = 0; a < np; ++a) {
     rbf_plan* p = g->parts[a];
-    const rbf::PushArgs& pa = g->push_args[a];
+    const rbf::PushArgs pa = g->push ? g->push_args[a] : rbf::PushArgs{};
     rbf::PartLoop& P = g->h_parts[a];
     const bool saved = p->push;
     p->push = false;  // plain streaming args (the part loop waits by itself)
@@ -441,7 +444,7 @@ int part_loop_prepare(rbf_group* g) {
     P.sys_scope = pa.sys_scope;
     P.my_flags = p->push_flags;
     P.wait_mask = 0;
-    for (int i = 0; i < p->wait_n; ++i) P.wait_mask |= 1ull << p->wait_ids[i];
+    for (int i = 0; g->push && i < p->wait_n; ++i) P.wait_mask |= 1ull << p->wait_ids[i];
     P.sync_row0 = std::min<int64_t>(p->halo_row0, first_push_row);
   }
   RBF_CK(cudaMalloc(&g->d_bars, sizeof(unsigned long long) * 3 * np));
