@@ -117,6 +117,8 @@ def main(args, metric, workloads):  # pragma: no cover - needs >1 GPU (or --forc
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     halo = torch.tensor([8 * sum(part.recv_count)], dtype=torch.int64)
     dist.all_reduce(halo, op=dist.ReduceOp.MAX)
+    stream = torch.tensor([float(plan.info()["stream_bytes_per_step"])], dtype=torch.float64)
+    dist.all_reduce(stream, op=dist.ReduceOp.SUM)  # bytes all ranks' loops stream per step
     n_rows_total = int(N - nb)
     peak = 6650.0
     try:
@@ -127,8 +129,7 @@ def main(args, metric, workloads):  # pragma: no cover - needs >1 GPU (or --forc
     if rank == 0:
         tmax = t.item()
         value = args.steps * n_rows_total / tmax
-        bytes_per_step = n_rows_total * (12 * n + 24)
-        per_gpu = bytes_per_step / world / (tmax / args.steps) / 1e9
+        per_gpu = stream.item() / world / (tmax / args.steps) / 1e9
         line = {
             "metric": metric, "value": value, "unit": "node-updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tmax / args.steps,
@@ -152,7 +153,8 @@ def main(args, metric, workloads):  # pragma: no cover - needs >1 GPU (or --forc
                        "setup_seconds": t_setup, "node_generation_seconds": t_nodes},
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s per GPU",
                          "frac": per_gpu / peak, "traffic": None,
-                         "bytes_formula": "N_i*(12n+24) / world (B(n), int32 ids)"},
+                         "bytes_formula": "bytes the ranks' loops stream per step (16-bit ids: 10n+24 per "
+                                          "row + 16 per slice; int32: 12n+24) / world"},
             "e2e": {"value": args.steps * n_rows_total / te.item(), "unit": "node-updates/s",
                     "h2d_bytes_per_step": 8 * N / args.steps, "d2h_bytes_per_step": 8 * N / args.steps},
             "gpu_launches": launches,
