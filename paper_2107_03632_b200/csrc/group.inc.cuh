@@ -103,7 +103,7 @@ struct rbf_group {
   rbf::TmaGeom part_geom = {1, 2, 0, 0};
   rbf::PartLoop* d_parts = nullptr;
   std::vector<rbf::PartLoop> h_parts;
-  unsigned long long* d_bars = nullptr;  // [3] per part
+  unsigned long long* d_bars = nullptr;  // [16] per part (one line each): arrivals, first bad step, residual
   std::vector<void*> part_bufs;          // push lists
 };
 
@@ -447,8 +447,10 @@ int part_loop_prepare(rbf_group* g) {
     for (int i = 0; g->push && i < p->wait_n; ++i) P.wait_mask |= 1ull << p->wait_ids[i];
     P.sync_row0 = std::min<int64_t>(p->halo_row0, first_push_row);
   }
-  RBF_CK(cudaMalloc(&g->d_bars, sizeof(unsigned long long) * 3 * np));
-  for (int a = 0; a < np; ++a) g->h_parts[a].bar = g->d_bars + 3 * a;
+  // one 128-byte line per part: a part's spinning CTAs must not share the
+  // line its neighbour's arrivals hit
+  RBF_CK(cudaMalloc(&g->d_bars, sizeof(unsigned long long) * 16 * np));
+  for (int a = 0; a < np; ++a) g->h_parts[a].bar = g->d_bars + 16 * a;
   RBF_CK(cudaMalloc(&g->d_parts, sizeof(rbf::PartLoop) * np));
   g->part_fn = fn;
   g->part_smem = p0->loop_smem;
@@ -465,8 +467,8 @@ int part_loop_upload(rbf_group* g) {
   for (int a = 0; a < np; ++a) g->h_parts[a].base = static_cast<unsigned long long>(g->parts[a]->push_base);
   RBF_CK(cudaMemcpyAsync(g->d_parts, g->h_parts.data(), sizeof(rbf::PartLoop) * np, cudaMemcpyHostToDevice,
                          g->stream));
-  std::vector<unsigned long long> bars(static_cast<size_t>(3 * np), 0ull);
-  for (int a = 0; a < np; ++a) bars[static_cast<size_t>(3 * a + 1)] = ~0ull;
+  std::vector<unsigned long long> bars(static_cast<size_t>(16 * np), 0ull);
+  for (int a = 0; a < np; ++a) bars[static_cast<size_t>(16 * a + 1)] = ~0ull;
   RBF_CK(cudaMemcpyAsync(g->d_bars, bars.data(), sizeof(unsigned long long) * bars.size(), cudaMemcpyHostToDevice,
                          g->stream));
   RBF_CK(cudaStreamSynchronize(g->stream));  // the host arrays above are pageable locals
@@ -533,6 +535,22 @@ int group_run_fast(rbf_group* g, int64_t limit, bool* any_bad, unsigned long lon
   RBF_CK(cudaEventRecord(g->ev1, g->stream));
   for (rbf_plan* p : g->parts) {
     if (g->push) p->push_base += limit;  // every part ran all `limit` pushes
+  }
+  if (fused && std::getenv("RBFFD_TRACE")) {  // RBFFD_TRACE: {-ncta, steps, [steps][ncta][4]} per part
+    RBF_CK(cudaStreamSynchronize(g->stream));
+    for (size_t a = 0; a < g->parts.size(); ++a) {
+      rbf_plan* p = g->parts[a];
+      if (!p->trace) continue;
+      const int64_t n_tr = std::min<int64_t>(limit, p->trace_cap), G = g->h_parts[a].ncta;
+      std::vector<unsigned long long> h(static_cast<size_t>(n_tr * G * 4));
+      RBF_CK(cudaMemcpy(h.data(), p->trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      if (std::FILE* f = std::fopen(std::getenv("RBFFD_TRACE"), "ab")) {
+        const int64_t hdr[2] = {-G, n_tr};
+        std::fwrite(hdr, sizeof(hdr), 1, f);
+        std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+        std::fclose(f);
+      }
+    }
   }
   // end-of-run reduction over all parts: min first-bad-step, max residual bits
   long long key = std::numeric_limits<long long>::max();

@@ -597,13 +597,22 @@ struct PartLoop {
   int n_nbr, my_id, sys_scope;
 };
 
+// Acquire polls at the scope of the neighbours (gpu: parts of this launch;
+// sys: parts on other GPUs).  A relaxed poll + one fence.acq_rel.sys was
+// measured slower (two in-process parts at C2: 33.9 vs 28.7 us per step).
 __device__ __forceinline__ void wait_arrivals(const unsigned long long* flags, unsigned long long mask,
-                                              unsigned long long need) {
+                                              unsigned long long need, int sys) {
   if ((threadIdx.x & 31) == 0) {
     const unsigned long long t0 = globaltimer();
     for (unsigned long long m = mask; m; m &= m - 1) {
       const int j = __ffsll(static_cast<long long>(m)) - 1;
-      while (ld_acquire_sys_u64(flags + j) < need) {
+      for (;;) {
+        unsigned long long v;
+        if (sys)
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + j) : "memory");
+        else
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + j) : "memory");
+        if (v >= need) break;
         __nanosleep(32);
         if (globaltimer() - t0 > 20000000000ull) __trap();
       }
@@ -623,6 +632,9 @@ part_loop_kernel(const PartLoop* __restrict__ parts, int n_parts, long long limi
   __shared__ long long s_issued;
   __shared__ unsigned long long s_max[32];
   __shared__ unsigned int s_bad[32];
+#ifdef RBF_TRACE
+  __shared__ unsigned long long s_wait;  // longest neighbour wait of a warp this step (ns)
+#endif
   int q_part = 0;
   while (q_part + 1 < n_parts && static_cast<int>(blockIdx.x) >= parts[q_part + 1].cta0) ++q_part;
   const PartLoop& P = parts[q_part];  // rarely used fields stay in global memory
@@ -702,6 +714,13 @@ part_loop_kernel(const PartLoop* __restrict__ parts, int n_parts, long long limi
     const bool need = step == limit - 1;
     bool bad = false, waited = wait_mask == 0ull;
     unsigned long long dmax = 0ull;
+#ifdef RBF_TRACE
+    unsigned long long tr0 = 0;
+    if (a.trace && ctid == 0) {
+      tr0 = globaltimer();
+      s_wait = 0;
+    }
+#endif
     const long long qbase = step * my_n;
     const long long qdiv = qbase / stages;
     const int qmod = static_cast<int>(qbase - qdiv * stages);
@@ -720,8 +739,14 @@ part_loop_kernel(const PartLoop* __restrict__ parts, int n_parts, long long limi
       const unsigned char* base = ring + static_cast<size_t>(s) * stage_bytes;
       const long long slice = (b + static_cast<long long>(i) * G) * sps + slot;
       if (!waited && (slice + 1) * 32 > sync_row0) {
-        wait_arrivals(my_flags, wait_mask, fbase + static_cast<unsigned long long>(step));
+#ifdef RBF_TRACE
+        const unsigned long long tw = globaltimer();
+#endif
+        wait_arrivals(my_flags, wait_mask, fbase + static_cast<unsigned long long>(step), sys_scope);
         waited = true;
+#ifdef RBF_TRACE
+        if (a.trace && lane == 0) atomicMax(&s_wait, globaltimer() - tw);
+#endif
       }
       const long long r = slice * 32 + lane;
       double value = 0.0;
@@ -788,6 +813,10 @@ part_loop_kernel(const PartLoop* __restrict__ parts, int n_parts, long long limi
       s_max[warp] = wm;
     }
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+#ifdef RBF_TRACE
+    unsigned long long tr1 = 0;
+    if (a.trace && ctid == 0) tr1 = globaltimer();
+#endif
     if (ctid == 0) {
       unsigned int cbad = 0;
       unsigned long long cm = 0ull;
@@ -800,26 +829,33 @@ part_loop_kernel(const PartLoop* __restrict__ parts, int n_parts, long long limi
       if (sys_scope) __threadfence_system();  // field stores and P2P pushes before the arrival
       else __threadfence();
       const unsigned long long target = static_cast<unsigned long long>(step + 1) * G;
-      const unsigned long long old = atomicAdd(&bar[0], 1ull);
-      if (old == target - 1) {  // last arriver of the part: tell the neighbours
-        const unsigned long long v = fbase + static_cast<unsigned long long>(step + 1);
+      atomicAdd(&bar[0], 1ull);  // no return value: a fire-and-forget reduction
+      unsigned long long v;
+      const unsigned long long t0 = globaltimer();
+      for (int spin = 0;; ++spin) {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&bar[0]) : "memory");
+        if (v >= target) break;
+        if ((spin & 1023) == 1023 && globaltimer() - t0 > 20000000000ull) __trap();
+      }
+      if (b == 0) {  // the part's step is complete: tell the neighbours
+        const unsigned long long fv = fbase + static_cast<unsigned long long>(step + 1);
         if (sys_scope) __threadfence_system();
-        else __threadfence();
         for (int j = 0; j < P.n_nbr; ++j) {
           if (sys_scope)
-            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.nbr_flags[j] + P.my_id), "l"(v) : "memory");
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.nbr_flags[j] + P.my_id), "l"(fv) : "memory");
           else
-            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(P.nbr_flags[j] + P.my_id), "l"(v) : "memory");
-        }
-      } else {
-        unsigned long long v;
-        const unsigned long long t0 = globaltimer();
-        for (int spin = 0;; ++spin) {
-          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&bar[0]) : "memory");
-          if (v >= target) break;
-          if ((spin & 1023) == 1023 && globaltimer() - t0 > 20000000000ull) __trap();
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(P.nbr_flags[j] + P.my_id), "l"(fv) : "memory");
         }
       }
+#ifdef RBF_TRACE
+      if (a.trace) {  // per step and CTA of the part: start, arrival, release, longest halo wait
+        unsigned long long* o = a.trace + ((step % a.trace_cap) * G + b) * 4;
+        o[0] = tr0;
+        o[1] = tr1;
+        o[2] = globaltimer();
+        o[3] = s_wait;
+      }
+#endif
     }
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
   }

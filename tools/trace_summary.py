@@ -33,7 +33,10 @@ def summarise_loop(t):
     print(f"  barrier (last arrival -> first release)   {us(rel.min(1) - arr.max(1))} us")
     print(f"  release spread (first -> last CTA)        {us(rel.max(1) - rel.min(1))} us")
     print(f"  CTA idle at the barrier, mean             {us((rel - arr).mean(1))} us")
-    print(f"  next-step chunks armed at arrival, mean   {np.median(ahead.mean(1)):7.2f}")
+    if ahead.max() > 1000:  # part loop traces: longest halo wait of a warp (ns)
+        print(f"  longest neighbour wait per CTA, mean / max {us(ahead.mean(1))} / {us(ahead.max(1))} us")
+    else:
+        print(f"  next-step chunks armed at arrival, mean   {np.median(ahead.mean(1)):7.2f}")
 
 
 def summarise(t):
