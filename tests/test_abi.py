@@ -104,7 +104,8 @@ def _sass_with_lines(tmp_path):
 
 
 UPDATE_KERNELS = ("step_tma_kernel", "step_stream_kernel", "grid_loop_kernel", "cluster_loop_kernel",
-                  "resident_loop_kernel", "pair_tma_kernel")
+                  "resident_loop_kernel", "pair_tma_kernel", "stream_loop_kernel", "part_loop_kernel")
+UNROLLED = ("step_tma_kernel", "stream_loop_kernel", "part_loop_kernel")
 
 
 def test_sass_is_native_sm100a_without_fma_in_the_update(tmp_path):
@@ -150,7 +151,11 @@ def test_sass_is_native_sm100a_without_fma_in_the_update(tmp_path):
                     assert where is not None and "__ddiv_rn" in src_line(*where), (name, where, line)
         m = re.search(r"ILi(\d+)E", name)
         nj = int(m.group(1)) if m else 0
-        if nj > 0 and "step_tma_kernel" in name:  # unrolled chain: nj products, nj + 2 sums
+        if nj > 0 and any(k in name for k in UNROLLED):  # unrolled chain: nj products, nj + 2 sums
             assert n_dmul >= nj and n_dadd >= nj + 2, (name, n_dmul, n_dadd)
-    assert checked >= 24 * 4, checked
-    assert any(k.startswith("_ZN3rbf15step_tma_kernelILi15ELi15ELi1ELi2E") for k in kernels)
+    assert checked >= 24 * 8, checked
+    # the production kernels of the benchmarked widths are among them
+    for k in ("_ZN3rbf15step_tma_kernelILi15ELi15ELi1ELi2E", "_ZN3rbf18stream_loop_kernelILi15ELi15ELi2E",
+              "_ZN3rbf18stream_loop_kernelILi30ELi15ELi2E", "_ZN3rbf18stream_loop_kernelILi56ELi8ELi4E",
+              "_ZN3rbf16part_loop_kernelILi15ELi15ELi2E"):
+        assert any(name.startswith(k) for name in kernels), k
