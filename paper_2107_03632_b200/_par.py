@@ -28,7 +28,8 @@ _pool = None
 def pool() -> ThreadPoolExecutor:
     global _pool
     if _pool is None:
-        _pool = ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1))
+        n = int(os.environ.get("RBFFD_HOST_THREADS", "0")) or min(32, os.cpu_count() or 1)
+        _pool = ThreadPoolExecutor(max_workers=max(1, n))
     return _pool
 
 
