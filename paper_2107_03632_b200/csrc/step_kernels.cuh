@@ -601,7 +601,7 @@ struct PartLoop {
 // sys: parts on other GPUs).  A relaxed poll + one fence.acq_rel.sys was
 // measured slower (two in-process parts at C2: 33.9 vs 28.7 us per step).
 __device__ __forceinline__ void wait_arrivals(const unsigned long long* flags, unsigned long long mask,
-                                              unsigned long long need, int sys) {
+                                              unsigned long long need, int sys, unsigned long long wait_ns) {
   if ((threadIdx.x & 31) == 0) {
     const unsigned long long t0 = globaltimer();
     for (unsigned long long m = mask; m; m &= m - 1) {
@@ -614,7 +614,7 @@ __device__ __forceinline__ void wait_arrivals(const unsigned long long* flags, u
           asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + j) : "memory");
         if (v >= need) break;
         __nanosleep(32);
-        if (globaltimer() - t0 > 20000000000ull) __trap();
+        if (globaltimer() - t0 > wait_ns) __trap();  // RBFFD_WAIT_TIMEOUT_MS (default 20 s)
       }
     }
   }
@@ -742,7 +742,7 @@ part_loop_kernel(const PartLoop* __restrict__ parts, int n_parts, long long limi
 #ifdef RBF_TRACE
         const unsigned long long tw = globaltimer();
 #endif
-        wait_arrivals(my_flags, wait_mask, fbase + static_cast<unsigned long long>(step), sys_scope);
+        wait_arrivals(my_flags, wait_mask, fbase + static_cast<unsigned long long>(step), sys_scope, a.wait_ns);
         waited = true;
 #ifdef RBF_TRACE
         if (a.trace && lane == 0) atomicMax(&s_wait, globaltimer() - tw);

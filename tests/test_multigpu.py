@@ -54,6 +54,29 @@ def test_partition_invariants(golden, name, P):
             assert (other.send_idx[j] >= other.n_boundary + other.n_halo).all()
 
 
+@pytest.mark.parametrize("name,P", [("crit6", 2), ("m6", 4)])
+def test_partition_row_groups(golden, name, P):
+    """Rows come in three groups -- neither reading a halo value nor read by
+    another part, read by another part only, reading a halo value -- each in
+    Morton order: the fused loop waits for its neighbours only from the first
+    row of the second group on (PartLoop::sync_row0)."""
+    nodes, shapes, interior, rows, f_int = _problem(golden, name)
+    parts = partition(nodes.n_total, interior, rows, shapes.weights, f_int, nodes.positions, P)
+    codes = morton_codes(nodes.positions[interior])
+    for p in parts:
+        base = p.n_boundary + p.n_halo
+        reads = ((p.rows >= p.n_boundary) & (p.rows < base)).any(axis=1)
+        sent = np.zeros(p.n_own, dtype=bool)
+        for idx in p.send_idx:
+            sent[idx - base] = True
+        group = np.where(reads, 2, np.where(sent, 1, 0))
+        assert (np.diff(group) >= 0).all(), p.rank
+        assert group.max() > 0, p.rank  # P > 1: every part exchanges something
+        for gid in range(3):
+            c = codes[p.rows_ref[group == gid]]
+            assert (np.diff(c.astype(np.int64)) >= 0).all(), (p.rank, gid)
+
+
 def test_morton_codes_order_locality():
     xy = np.array([[0.0, 0.0], [1.0, 1.0], [0.0, 1.0], [1.0, 0.0]])
     c = morton_codes(xy)
