@@ -396,7 +396,7 @@ int part_loop_prepare(rbf_group* g) {
     P.ncta = ncta[a];
     cta0 += ncta[a];
     // per-slice push lists from the part's send segments
-    std::vector<int> cnt(static_cast<size_t>(p->S) + 1, 0);
+    std::vector<int64_t> cnt(static_cast<size_t>(p->S) + 1, 0);
     std::vector<unsigned long long> ent;
     int64_t first_push_row = p->N_i;
     for (int i = 0; i < pa.n_peer; ++i) {
@@ -409,10 +409,9 @@ int part_loop_prepare(rbf_group* g) {
     }
     for (int64_t sl = 0; sl < p->S; ++sl) cnt[static_cast<size_t>(sl) + 1] += cnt[static_cast<size_t>(sl)];
     if (cnt.back() > 0) {
-      if (static_cast<int64_t>(cnt.back()) >= (int64_t(1) << 31))
-        return RBF_OK;
+      if (cnt.back() >= (int64_t(1) << 31)) return RBF_OK;  // int32 per-slice offsets
       ent.assign(static_cast<size_t>(cnt.back()), 0ull);
-      std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+      std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
       for (int i = 0; i < pa.n_peer; ++i) {
         for (int64_t k = pa.peer[i].src_off; k < pa.peer[i].src_off + pa.peer[i].count; ++k) {
           const int64_t row = static_cast<int64_t>(p->halo_send_idx_h[static_cast<size_t>(k)]) - p->B;
@@ -423,13 +422,14 @@ int part_loop_prepare(rbf_group* g) {
               (static_cast<unsigned long long>(i) << 58) | (static_cast<unsigned long long>(row & 31) << 52) | slot;
         }
       }
+      const std::vector<int> off(cnt.begin(), cnt.end());
       int* d_off = nullptr;
       unsigned long long* d_ent = nullptr;
-      RBF_CK(cudaMalloc(&d_off, sizeof(int) * cnt.size()));
+      RBF_CK(cudaMalloc(&d_off, sizeof(int) * off.size()));
       g->part_bufs.push_back(d_off);
       RBF_CK(cudaMalloc(&d_ent, sizeof(unsigned long long) * ent.size()));
       g->part_bufs.push_back(d_ent);
-      RBF_CK(cudaMemcpy(d_off, cnt.data(), sizeof(int) * cnt.size(), cudaMemcpyHostToDevice));
+      RBF_CK(cudaMemcpy(d_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice));
       RBF_CK(cudaMemcpy(d_ent, ent.data(), sizeof(unsigned long long) * ent.size(), cudaMemcpyHostToDevice));
       P.push_off = d_off;
       P.push_ent = d_ent;
