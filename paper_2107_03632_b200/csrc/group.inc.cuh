@@ -451,28 +451,7 @@ int part_loop_prepare(rbf_group* g) {
   // line its neighbour's arrivals hit
   RBF_CK(cudaMalloc(&g->d_bars, sizeof(unsigned long long) * 16 * np));
   for (int a = 0; a < np; ++a) g->h_parts[a].bar = g->d_bars + 16 * a;
-  // descriptors, then the CTA -> (part, part CTA) table: parts interleaved
-  // over the launch in proportion to their CTA counts
-  std::vector<int2> cmap(static_cast<size_t>(cta0));
-  {
-    std::vector<int> given(np, 0);
-    for (int i = 0; i < cta0; ++i) {
-      int best = -1;
-      double best_def = -1e300;
-      for (int a = 0; a < np; ++a) {
-        if (given[a] >= ncta[a]) continue;
-        const double def = static_cast<double>(ncta[a]) * (i + 1) / cta0 - given[a];
-        if (def > best_def) {
-          best_def = def;
-          best = a;
-        }
-      }
-      cmap[static_cast<size_t>(i)] = make_int2(best, given[best]++);
-    }
-  }
-  RBF_CK(cudaMalloc(&g->d_parts, sizeof(rbf::PartLoop) * np + sizeof(int2) * cmap.size()));
-  RBF_CK(cudaMemcpy(reinterpret_cast<unsigned char*>(g->d_parts) + sizeof(rbf::PartLoop) * np, cmap.data(),
-                    sizeof(int2) * cmap.size(), cudaMemcpyHostToDevice));
+  RBF_CK(cudaMalloc(&g->d_parts, sizeof(rbf::PartLoop) * np));
   g->part_fn = fn;
   g->part_smem = p0->loop_smem;
   g->part_grid = cta0;

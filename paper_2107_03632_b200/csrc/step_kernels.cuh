@@ -567,7 +567,7 @@ stream_loop_kernel(StepArgs a, LoopArgs L, TmaGeom g) {
 // ---------------------------------------------------------------------------
 // Partitioned persistent loop (fixed-step fast path of a
 // push-mode group): every local part of the group runs the streaming loop
-// above on its own CTAs of ONE cooperative launch, and the halo exchange
+// above on its own CTA range of ONE cooperative launch, and the halo exchange
 // is fused into it.  A row whose value a neighbour part reads is stored
 // straight into the neighbour's field buffer (its halo slot in the buffer the
 // neighbour reads next step: P2P stores over NVLink when the neighbour is
@@ -584,7 +584,7 @@ stream_loop_kernel(StepArgs a, LoopArgs L, TmaGeom g) {
 struct PartLoop {
   StepArgs a;                 // W / C16 / C / meta / F / n_rows / dst_base / st of the part
   double* U[2];               // the part's field buffers (start field in U[0])
-  int cta0, ncta;             // CTAs of the part (cta0: first index of its range before interleaving)
+  int cta0, ncta;             // CTA range of the part in the launch
   long long sync_row0;        // first row that reads a halo value or is pushed
   unsigned long long* bar;    // [0] arrival counter, [1] first non-finite step (min), [2] residual bits (max)
   const int* push_off;        // [S+1] per-slice ranges of push_ent (nullptr: no pushes)
@@ -596,7 +596,6 @@ struct PartLoop {
   unsigned long long base;    // arrival count before this run (steps pushed in earlier runs)
   int n_nbr, my_id, sys_scope;
 };
-static_assert(sizeof(PartLoop) % alignof(int2) == 0, "the CTA table follows the descriptors");
 
 // Acquire polls at the scope of the neighbours (gpu: parts of this launch;
 // sys: parts on other GPUs).  A relaxed poll + one fence.acq_rel.sys was
@@ -636,11 +635,8 @@ part_loop_kernel(const PartLoop* __restrict__ parts, int n_parts, long long limi
 #ifdef RBF_TRACE
   __shared__ unsigned long long s_wait;  // longest neighbour wait of a warp this step (ns)
 #endif
-  // CTA -> (part, CTA of the part): the table after the descriptors spreads
-  // every part's CTAs over the whole launch (both dies), so a part's barrier
-  // line is as near to its CTAs on average as the single loop's
-  const int2 cmap = reinterpret_cast<const int2*>(parts + n_parts)[blockIdx.x];
-  const int q_part = cmap.x;
+  int q_part = 0;
+  while (q_part + 1 < n_parts && static_cast<int>(blockIdx.x) >= parts[q_part + 1].cta0) ++q_part;
   const PartLoop& P = parts[q_part];  // rarely used fields stay in global memory
   const StepArgs a = P.a;
   double* const U0 = P.U[0];
@@ -652,7 +648,7 @@ part_loop_kernel(const PartLoop* __restrict__ parts, int n_parts, long long limi
   const unsigned long long wait_mask = P.wait_mask, fbase = P.base;
   unsigned long long* const bar = P.bar;
   const int sys_scope = P.sys_scope;
-  const int G = P.ncta, b = cmap.y;
+  const int G = P.ncta, b = static_cast<int>(blockIdx.x) - P.cta0;
   const int sps = g.sps, stages = g.stages;
   const int wbytes = sps * NJ * 32 * 8, cbytes = sps * NJ * 32 * IB;
   const int stage_bytes = sps * tma_slice_bytes<NJ, IB>();
