@@ -936,7 +936,6 @@ int launch_assemble(const double* d_pos, const int* d_rows, long long cnt, long 
   wa.bad_row = d_bad;
   wa.status = d_status;
   wa.n_flagged = d_nflag;
-  const int S = n + wa.M;
   const size_t per_warp = rbf::assemble_smem_doubles(n, wa.M) * sizeof(double);
   int warps = static_cast<int>(std::min<size_t>(8, (200 * 1024) / per_warp));
   if (warps < 1) return fail(RBF_ERR_PARAM, "support too large for on-chip weight assembly");
