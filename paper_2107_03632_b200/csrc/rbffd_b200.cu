@@ -1222,7 +1222,14 @@ int finish_plan(std::unique_ptr<rbf_plan>& p, uint32_t flags) {
                                                                                  int64_t(sms) * occ)));
         int lres = 0;
         if (const char* e = std::getenv("RBFFD_LOOP_RES")) lres = std::max(0, std::atoi(e));
-        p->loop_geom = rbf::TmaGeom{lsps, stages, 0, lres};
+        // L2 policy of the stream: evict_first keeps the field buffers
+        // L2-resident while they fit (C2: 24.7 us vs 29.3 with evict_normal);
+        // once they do not, evict_normal is 0.7 % faster with 16-bit ids
+        // (m=2 N=1e7 260.0 vs 261.8 us, C3 480.0 vs 483.5) and 0.9 % slower
+        // with int32 ids (C4 2.600 vs 2.576 ms): profiles/r02/loop_policy_ab.log
+        int lpol = (p->index_bits == 16 && 16 * N > (int64_t(64) << 20)) ? 1 : 0;
+        if (const char* e = std::getenv("RBFFD_LOOP_POLICY")) lpol = std::max(0, std::min(2, std::atoi(e)));
+        p->loop_geom = rbf::TmaGeom{lsps, stages, lpol, lres};
       }
     }
     cudaGetLastError();

@@ -343,7 +343,12 @@ stream_loop_kernel(StepArgs a, LoopArgs L, TmaGeom g) {
     if (lane == 0) {
       // chunks i < g.res of every step are streamed with L2::evict_last and
       // stay L2-resident across steps; the rest with evict_first
-      const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+      // g.contig (unused by this kernel's geometry) selects the stream's L2
+      // policy for experiments: 0 evict_first (default), 1 evict_normal,
+      // 2 evict_unchanged (RBFFD_LOOP_POLICY)
+      const uint64_t pol_first = g.contig == 1 ? policy_evict_normal()
+                                 : g.contig == 2 ? policy_evict_unchanged() : policy_evict_first();
+      const uint64_t pol_last = policy_evict_last();
       int i = 0, s = 0;
       uint32_t ph = 1;  // empty-barrier parity of the stage's previous occupant
       long long q = 0;
