@@ -1699,17 +1699,70 @@ __device__ __forceinline__ unsigned long long spread_bits21(unsigned long long v
   v = (v | (v << 1)) & 0x5555555555555555ull;
   return v;
 }
+// Bounding box of the node positions for the Morton quantisation, on the
+// device (min / max are exact: the same values as a host pass).
+// partial[4 * block] = {xmin, xmax, ymin, ymax}; finish with one block.
+__global__ void __launch_bounds__(256) bounds_partial_kernel(const double* __restrict__ pos, long long n,
+                                                             double* __restrict__ partial) {
+  double a0 = 1e300, a1 = -1e300, b0 = 1e300, b1 = -1e300;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double x = pos[2 * i], y = pos[2 * i + 1];
+    a0 = fmin(a0, x);
+    a1 = fmax(a1, x);
+    b0 = fmin(b0, y);
+    b1 = fmax(b1, y);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a0 = fmin(a0, __shfl_xor_sync(0xffffffffu, a0, o));
+    a1 = fmax(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+    b0 = fmin(b0, __shfl_xor_sync(0xffffffffu, b0, o));
+    b1 = fmax(b1, __shfl_xor_sync(0xffffffffu, b1, o));
+  }
+  __shared__ double s[8][4];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s[w][0] = a0;
+    s[w][1] = a1;
+    s[w][2] = b0;
+    s[w][3] = b1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) {
+      a0 = fmin(a0, s[k][0]);
+      a1 = fmax(a1, s[k][1]);
+      b0 = fmin(b0, s[k][2]);
+      b1 = fmax(b1, s[k][3]);
+    }
+    partial[4 * blockIdx.x + 0] = a0;
+    partial[4 * blockIdx.x + 1] = a1;
+    partial[4 * blockIdx.x + 2] = b0;
+    partial[4 * blockIdx.x + 3] = b1;
+  }
+}
 // key[k] = Morton code of interior node k's position (21 bits per axis over
-// the bounding box), val[k] = k; a stable radix sort of (key, val) orders the
-// rows by (code, k)
-__global__ void morton_keys_kernel(const double* __restrict__ pos, const long long* __restrict__ interior,
-                                   long long n_rows, double xmin, double ymin, double sx, double sy,
-                                   unsigned long long* __restrict__ key, long long* __restrict__ val) {
+// the bounding box from bounds_partial_kernel's `nb` partials; the IEEE
+// expression of multigpu.morton_codes), val[k] = k; a stable radix sort of
+// (key, val) orders the rows by (code, k).
+__global__ void morton_keys_dev_kernel(const double* __restrict__ pos, const long long* __restrict__ interior,
+                                       long long n_rows, const double* __restrict__ partial, int nb,
+                                       unsigned long long* __restrict__ key, long long* __restrict__ val) {
+  double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
+  for (int k = 0; k < nb; ++k) {
+    xmin = fmin(xmin, partial[4 * k + 0]);
+    xmax = fmax(xmax, partial[4 * k + 1]);
+    ymin = fmin(ymin, partial[4 * k + 2]);
+    ymax = fmax(ymax, partial[4 * k + 3]);
+  }
+  const double sx = (xmax > xmin) ? __ddiv_rn(2097151.0, __dsub_rn(xmax, xmin)) : 0.0;
+  const double sy = (ymax > ymin) ? __ddiv_rn(2097151.0, __dsub_rn(ymax, ymin)) : 0.0;
   for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n_rows;
        k += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long v = interior[k];
-    const unsigned long long qx = static_cast<unsigned int>((pos[2 * v] - xmin) * sx);
-    const unsigned long long qy = static_cast<unsigned int>((pos[2 * v + 1] - ymin) * sy);
+    const unsigned long long qx = static_cast<unsigned int>(__dmul_rn(__dsub_rn(pos[2 * v], xmin), sx));
+    const unsigned long long qy = static_cast<unsigned int>(__dmul_rn(__dsub_rn(pos[2 * v + 1], ymin), sy));
     key[k] = spread_bits21(qx) | (spread_bits21(qy) << 1);
     val[k] = k;
   }
